@@ -1,0 +1,250 @@
+/*
+ * inr.h — C ABI of the B200 (sm_100a) hash-grid INR library `libinr.so`.
+ *
+ * The operation is the hot path of arXiv 2304.10516 ("distributed neural
+ * representation", DNR): one implicit neural representation per spatial block
+ * of a scalar volume,
+ *     Phi : R^3 -> R^D, (x,y,z) -> v                    (Eq. 1)
+ * built from a multiresolution hash-grid encoding and a small ReLU MLP
+ * (PAPER.md L157-158, L217-218), fitted to uniformly sampled, interpolated and
+ * normalized targets (L172-173, L204-205) with the boundary-weighted L1 loss
+ *     L = (1 - lambda) L1(X_Uniform, Y_Uniform) + lambda L1(X_Bound, Y_Bound)
+ * (Eq. 2) and Adam with a step learning-rate schedule (L220), then
+ * decoded by coordinate query or to a grid (L175-176, L268), and cached in a
+ * FIFO window of timesteps (L238, L271-274, L290).  Where the paper is silent
+ * the readings R1..R25 of DESIGN.md apply; they are cited below as [Rn].
+ *
+ * Conventions
+ *  - Every function returns an inr_status and never aborts or throws.  On a
+ *    non-OK status, inr_last_error() returns thread-local text describing it.
+ *  - All pointers marked (dev) are device pointers on the model's device; the
+ *    caller owns them and keeps them valid until the stream has executed the
+ *    call's work.  The library never retains caller buffers.  (host) pointers
+ *    are ordinary host memory.
+ *  - The library owns everything behind handles: tables, MLP weights, grads,
+ *    Adam state, workspaces.
+ *  - Coordinates are (x, y, z); volumes are x-fastest, then y, then z.
+ *  - A block with core origin o and n cells per axis maps node position p to
+ *    the block-normalized x = (p - o)/n in [0,1]^3 (cell-span convention, so
+ *    neighbouring blocks share the face plane o + n) [R5].
+ *  - Sticky CUDA errors surface as INR_ERR_CUDA at the next call.
+ *  - There is no CPU fallback: without a usable sm_100 device every call that
+ *    needs one fails with INR_ERR_CUDA.
+ */
+#ifndef INR_H
+#define INR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define INR_API __attribute__((visibility("default")))
+#else
+#define INR_API
+#endif
+
+typedef struct CUstream_st* cudaStream_t;  /* identical to the CUDA runtime typedef */
+
+typedef enum {
+  INR_OK = 0,
+  INR_ERR_INVALID_ARG = 1,   /* null handle, bad config or option, steps < 1, ... */
+  INR_ERR_DOMAIN = 2,        /* strict decode: a coordinate outside [0, N-1]^3 */
+  INR_ERR_NONFINITE = 3,     /* non-finite loss or parameter detected after a step */
+  INR_ERR_OOM = 4,
+  INR_ERR_CUDA = 5,
+  INR_ERR_STATE = 6,         /* evict on empty cache; fit on a frozen (cached) model */
+  INR_ERR_UNSUPPORTED = 7    /* a valid configuration outside this build's kernels */
+} inr_status;
+
+/* Thread-local text of the last non-OK status of this thread ("" if none). */
+INR_API const char* inr_last_error(void);
+
+enum { INR_PREC_FP32 = 0,      /* MLP on CUDA cores in fp32 (parity mode) */
+       INR_PREC_FP16_MLP = 1   /* MLP on tcgen05 tensor cores: fp16 operands, fp32
+                                  accumulate in TMEM, fp32 master weights [R17] */ };
+enum { INR_REDUCE_ATOMIC = 0,          /* fp32 atomics: fastest, run-to-run rounding noise */
+       INR_REDUCE_DETERMINISTIC = 1 }; /* exact int64 fixed-point sums: bitwise reproducible [R21] */
+
+/* Network configuration.
+ *   levels L >= 1, features F in {1,2,4,8}, table size T = 2^log2_table_size
+ *   (1..24), base resolution N_min >= 1, per_level_scale b > 1; level l has
+ *   resolution N_l = floor(N_min * b^l) [R3] and min(T, (N_l+1)^3) entries
+ *   (dense x-fastest index when (N_l+1)^3 <= T, else the spatial hash of S:L236) [R1, R2].
+ *   mlp_width W = 64 (this build), mlp_hidden_layers H in 1..8 (H hidden layers
+ *   => H+1 weight matrices [R16]), out_dim D = 1, mlp_bias in {0,1} [R15].
+ *   L*F <= 64 and, for INR_PREC_FP16_MLP, a multiple of 16.
+ *   seed selects the Philox4x32-10 streams for init (0), uniform samples (1),
+ *   boundary samples (2) [R8, R14]. */
+typedef struct {
+  int32_t levels, features, log2_table_size, base_resolution;
+  float per_level_scale;
+  int32_t mlp_width, mlp_hidden_layers, out_dim, mlp_bias;
+  int32_t precision, reduction;
+  uint64_t seed;
+} inr_config;
+
+/* A block (partition core) of a volume, in node units.
+ * origin[d] is a multiple of n[d]; the volume has global_dims[d] nodes; blocks
+ * tile it with ceil(N/n) blocks per axis; block id = (bz*By + by)*Bx + bx. */
+typedef struct {
+  int64_t origin[3];
+  int32_t n[3];
+  int64_t global_dims[3];
+} inr_block;
+
+typedef struct inr_model inr_model;  /* opaque; lives on one CUDA device */
+
+/* Allocate a model on `device` and initialise it from cfg->seed [R14]
+ * (tables U[-1e-4,1e-4], weights He-uniform, biases 0; Philox stream 0,
+ * counter (param index j, block id, 0, 0)).  Errors: INVALID_ARG, UNSUPPORTED,
+ * OOM, CUDA. */
+INR_API inr_status inr_create(const inr_config* cfg, const inr_block* block, int device, inr_model** out);
+/* Re-initialise parameters from `seed`, zero Adam state and grads, step = 0
+ * (fresh init per timestep, [R22]).  INR_ERR_STATE on a frozen model. */
+INR_API inr_status inr_reset(inr_model* m, uint64_t seed);
+/* Free a model (NULL is a no-op).  Models borrowed from a cache must not be destroyed. */
+INR_API inr_status inr_destroy(inr_model* m);
+/* Number of fp32 parameters in the declared order (tables by level, then
+ * W_0, b_0, ..., W_H, b_H) and the stored bytes (4 per parameter) [R24]. */
+INR_API inr_status inr_param_count(const inr_model* m, int64_t* count);
+INR_API inr_status inr_param_bytes(const inr_model* m, int64_t* bytes);
+/* Adam steps taken so far. */
+INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
+
+/* Fit options.  Defaults in
+ * inr_fit_opts_default(): lambda 0.5, boundary_batch 0, lr0 1e-2, lr_decay 0.8,
+ * lr_step 500, beta1 0.9, beta2 0.999, eps 1e-8, vmin 0, vmax 1,
+ * target_psnr 0, check_interval 0.
+ *   lambda in [0,1]; boundary_batch B_b >= 0 boundary samples per step (lambda'
+ *   = 0 when B_b = 0 or the block has no interior face [R11]); lr at 0-based
+ *   step s is lr0 * lr_decay^floor(s / lr_step) [R13]; Adam is PyTorch's dense
+ *   form [R12]; [vmin, vmax] is the global value range shared by all blocks
+ *    — vmax == vmin is legal (targets 0, report.constant_field = 1);
+ *   target_psnr > 0 with check_interval > 0 stops once the PSNR on a 32^3
+ *   cell-centred probe lattice reaches the target. */
+typedef struct {
+  float lambda;
+  int32_t boundary_batch;
+  float lr0, lr_decay;
+  int32_t lr_step;
+  float beta1, beta2, eps;
+  float vmin, vmax;
+  float target_psnr;
+  int32_t check_interval;
+} inr_fit_opts;
+INR_API void inr_fit_opts_default(inr_fit_opts* o);
+
+typedef struct {
+  int32_t steps_taken, reached_target, constant_field;
+  double loss_uniform, loss_boundary;  /* Eq. 2 terms of the last step taken */
+  double probe_psnr;                   /* last probe PSNR (dB), 0 if never probed */
+} inr_fit_report;
+
+/* Strided device view of fp32 node values: node (i,j,k) of the volume (global
+ * indices, lo[d] <= i < lo[d] + dims[d]) is base[(i-lo0)*stride0 + (j-lo1)*stride1
+ * + (k-lo2)*stride2] (strides in elements).  For a block it must cover nodes
+ * [o_d, min(o_d + n_d, N_d - 1)] per axis (the core plus the 1-node high-side
+ * ghost layer [R6]); many blocks may share one allocation (zero-copy). */
+typedef struct {
+  const float* base;
+  int64_t lo[3];
+  int32_t dims[3];
+  int64_t stride[3];
+} inr_view;
+
+/* Train one model for `steps` >= 1 steps of `batch` >= 1 uniform samples plus
+ * opts->boundary_batch boundary samples: Philox samples,
+ * trilinear targets from the view, encode, MLP forward, Eq. 2, MLP backward,
+ * table scatter-add, Adam.  Parameters continue from the model's current
+ * step.  If `out` is non-NULL the call synchronizes `stream` and fills the
+ * report (INR_ERR_NONFINITE if a non-finite loss/parameter appeared); if `out`
+ * is NULL the call is stream-ordered and asynchronous (no probe stopping).
+ * The gradients of the last step stay readable through inr_get_grads. */
+INR_API inr_status inr_fit(inr_model* m, const inr_view* block_values, int32_t steps, int32_t batch,
+                   const inr_fit_opts* opts, inr_fit_report* out, cudaStream_t stream);
+/* Same semantics for `nmodels` independent models (one block each, all with the
+ * same inr_config and device) in one fused launch per kernel per step
+ * (decentralized DNR: no communication between models).  `out`,
+ * if non-NULL, is an array of nmodels reports. */
+INR_API inr_status inr_fit_group(inr_model* const* models, const inr_view* views, int32_t nmodels,
+                         int32_t steps, int32_t batch, const inr_fit_opts* opts,
+                         inr_fit_report* out, cudaStream_t stream);
+
+/* Direct queries: xyz (dev) holds q global node
+ * coordinates (x,y,z interleaved); out (dev) receives q values in data units
+ * v = Phi(x) (vmax - vmin) + vmin.  A query p goes to the block
+ * min(max(floor(p/n), 0), B-1) per axis and x = fl32(fl32(p - o)/n) [R5];
+ * inr_decode uses the one model, inr_decode_group routes among `nmodels`
+ * models (a point whose block is not among them gets NaN).  strict != 0
+ * reports INR_ERR_DOMAIN after the fact if any coordinate lies outside
+ * [0, N-1]^3 (values are still written, clamped); strict synchronizes. */
+INR_API inr_status inr_decode(const inr_model* m, const float* xyz, int64_t q, float* out, int32_t strict,
+                      cudaStream_t stream);
+INR_API inr_status inr_decode_group(const inr_model* const* models, int32_t nmodels, const float* xyz,
+                            int64_t q, float* out, int32_t strict, cudaStream_t stream);
+
+/* Decode to grid: res[d] >= 1 samples per axis at
+ * x_j = fl32(j / res_d), j < res_d (half-open, so blocks tile without
+ * duplicates [R19]); value written to out[jx*os0 + jy*os1 + jz*os2] where
+ * os = out_stride (elements) or, if out_stride is NULL, the dense x-fastest
+ * strides (1, res0, res0*res1).  If ref (dev, same layout) is non-NULL, the
+ * sum over the lattice of ((pred - ref)/(vmax - vmin))^2 is atomically added
+ * to *sse_dev (dev double; caller zeroes it; many blocks may accumulate into
+ * one scalar) (S:L75-83 PSNR in normalized units [R18]).  Asynchronous. */
+INR_API inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
+                           const int64_t* out_stride, const float* ref, double* sse_dev,
+                           cudaStream_t stream);
+
+/* Min/max over the nodes of a view: atomically
+ * folds into minmax_dev[0] (min) and minmax_dev[1] (max) (dev floats, caller
+ * initialises to +inf/-inf).  The cross-GPU all-reduce is the caller's. */
+INR_API inr_status inr_value_range(const inr_view* view, float* minmax_dev, cudaStream_t stream);
+
+/* ---- the temporal window ---- */
+typedef struct inr_cache inr_cache;
+/* capacity >= 1 timesteps; host_resident != 0 keeps snapshots in pinned host
+ * memory ("cached in system RAM") and stages them to the device on
+ * decode; otherwise snapshots stay in device memory. */
+INR_API inr_status cache_create(int32_t capacity, int32_t host_resident, int device, inr_cache** out);
+INR_API inr_status cache_destroy(inr_cache* c);
+/* Copy a frozen parameter snapshot (no optimizer state) of `nblocks`
+ * models as timestep `timestep` (> every cached timestep); when full,
+ * the oldest timestep is evicted first and reported in *evicted_timestep
+ * (-1 if none).  The source models stay usable.  Stream-ordered. */
+INR_API inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* const* blocks, int32_t nblocks,
+                        int64_t* evicted_timestep, cudaStream_t stream);
+/* Evict the oldest timestep (INR_ERR_STATE if empty). */
+INR_API inr_status cache_evict(inr_cache* c, int64_t* evicted_timestep);
+INR_API inr_status cache_size(const inr_cache* c, int32_t* n);
+/* Snapshot bytes currently held (device or host). */
+INR_API inr_status cache_bytes(const inr_cache* c, int64_t* bytes);
+/* Borrow slot i (0 = oldest): its timestep and frozen models (decode only;
+ * valid until that slot is evicted; inr_fit/inr_reset on them -> INR_ERR_STATE). */
+INR_API inr_status cache_get(const inr_cache* c, int32_t i, int64_t* timestep, const inr_model* const** blocks,
+                     int32_t* nblocks);
+
+/* ---- parity / test surface ---- */
+/* Copy n = inr_param_count floats of parameters / last-step gradients / Adam m /
+ * Adam v in the declared order (synchronous). */
+INR_API inr_status inr_get_params(const inr_model* m, float* host, int64_t n);
+INR_API inr_status inr_set_params(inr_model* m, const float* host, int64_t n);
+INR_API inr_status inr_get_grads(const inr_model* m, float* host, int64_t n);
+INR_API inr_status inr_get_adam_state(const inr_model* m, float* m_host, float* v_host, int64_t n);
+/* Encode q block-normalized coordinates x01 (dev, q x 3): corner indices
+ * idx (dev, q x L x 8 uint32, level-local table index) and/or features
+ * feat (dev, q x L*F fp32); either may be NULL.  Asynchronous. */
+INR_API inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_t q, uint32_t* idx, float* feat,
+                            cudaStream_t stream);
+/* Network output Phi(x) in normalized units for q block-normalized coordinates
+ * (dev q x 3 -> dev q), in the model's configured precision.  Asynchronous. */
+INR_API inr_status inr_debug_forward(const inr_model* m, const float* x01, int64_t q, float* y, cudaStream_t stream);
+/* Number of kernels this library has launched since load (bench evidence). */
+INR_API int64_t inr_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INR_H */

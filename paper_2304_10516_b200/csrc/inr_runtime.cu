@@ -1,0 +1,801 @@
+// inr_runtime.cu — host runtime behind the C ABI of include/inr.h.
+//
+// Owns model memory (parameters, gradients, Adam state, counters: one device
+// allocation per model), builds the per-group kernel parameter blocks, runs the
+// fit loop (optionally as a replayed CUDA graph per step), dispatches decode,
+// and implements the FIFO timestep window.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/inr.h"
+#include "launch.h"
+
+using namespace inr;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+namespace inr {
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}
+
+static inr_status fail(inr_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+static inr_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) return fail(INR_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+  return fail(INR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call)                                        \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+#define CK_LAUNCH(what)                                  \
+  do {                                                   \
+    cudaError_t e_ = cudaGetLastError();                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);   \
+  } while (0)
+
+extern "C" const char* inr_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t inr_kernel_launches(void) { return g_launches.load(); }
+
+// ------------------------------------------------------------------ model
+struct inr_model {
+  inr_config cfg;
+  inr_block blk;
+  int device;
+  NetDesc net;
+  int64_t P;            // parameters
+  int64_t P_pad;        // padded stride of each array
+  void* mem = nullptr;
+  float* params = nullptr;
+  float* grads = nullptr;
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  unsigned long long* gfx = nullptr;
+  long long* step_total = nullptr;
+  long long* step_cur = nullptr;
+  double* acc = nullptr;
+  int* flag = nullptr;
+  int64_t steps = 0;
+  uint32_t block_id = 0;
+  int nfaces = 0;
+  int faces[6] = {0, 0, 0, 0, 0, 0};
+  float vmin = 0.f, vmax = 1.f;
+  bool frozen = false;       // cache snapshot: parameters only
+  bool host_resident = false;
+  float* host_params = nullptr;  // pinned copy (host-resident snapshot)
+  bool staged = false;           // params (device) holds the host copy
+};
+
+static inr_status validate_config(const inr_config* c) {
+  if (!c) return fail(INR_ERR_INVALID_ARG, "config is NULL");
+  if (c->levels < 1) return fail(INR_ERR_INVALID_ARG, "levels must be >= 1");
+  if (c->features < 1) return fail(INR_ERR_INVALID_ARG, "features must be >= 1");
+  if (c->log2_table_size < 1 || c->log2_table_size > 30)
+    return fail(INR_ERR_INVALID_ARG, "log2_table_size must be in 1..30 (T a power of two)");
+  if (c->base_resolution < 1) return fail(INR_ERR_INVALID_ARG, "base_resolution must be >= 1");
+  if (!(c->per_level_scale > 1.f)) return fail(INR_ERR_INVALID_ARG, "per_level_scale must be > 1");
+  if (c->mlp_hidden_layers < 1) return fail(INR_ERR_INVALID_ARG, "mlp_hidden_layers must be >= 1");
+  if (c->mlp_width < 1) return fail(INR_ERR_INVALID_ARG, "mlp_width must be >= 1");
+  if (c->out_dim < 1) return fail(INR_ERR_INVALID_ARG, "out_dim must be >= 1");
+  if (c->precision != INR_PREC_FP32 && c->precision != INR_PREC_FP16_MLP)
+    return fail(INR_ERR_INVALID_ARG, "unknown precision");
+  if (c->reduction != INR_REDUCE_ATOMIC && c->reduction != INR_REDUCE_DETERMINISTIC)
+    return fail(INR_ERR_INVALID_ARG, "unknown reduction");
+  if (c->features != 1 && c->features != 2 && c->features != 4 && c->features != 8)
+    return fail(INR_ERR_UNSUPPORTED, "features must be 1, 2, 4 or 8 in this build");
+  if (c->levels > kMaxLevels) return fail(INR_ERR_UNSUPPORTED, "at most %d levels", kMaxLevels);
+  if (c->levels * c->features > 64) return fail(INR_ERR_UNSUPPORTED, "levels*features must be <= 64");
+  if (c->log2_table_size > 24) return fail(INR_ERR_UNSUPPORTED, "log2_table_size must be <= 24 in this build");
+  if (c->mlp_width != kWidth) return fail(INR_ERR_UNSUPPORTED, "mlp_width must be 64 in this build");
+  if (c->mlp_hidden_layers > kMaxLayers - 1) return fail(INR_ERR_UNSUPPORTED, "at most 8 hidden layers");
+  if (c->out_dim != 1) return fail(INR_ERR_UNSUPPORTED, "out_dim must be 1 in this build");
+  if (c->precision == INR_PREC_FP16_MLP && (c->levels * c->features) % 16 != 0)
+    return fail(INR_ERR_UNSUPPORTED, "fp16 MLP needs levels*features to be a multiple of 16");
+  return INR_OK;
+}
+
+static inr_status validate_block(const inr_block* b) {
+  if (!b) return fail(INR_ERR_INVALID_ARG, "block is NULL");
+  for (int d = 0; d < 3; ++d) {
+    if (b->n[d] < 1 || b->global_dims[d] < 1 || b->origin[d] < 0)
+      return fail(INR_ERR_INVALID_ARG, "block extents must be positive");
+    if (b->origin[d] % b->n[d] != 0) return fail(INR_ERR_INVALID_ARG, "block origin must be a multiple of n");
+    if (b->origin[d] >= b->global_dims[d]) return fail(INR_ERR_INVALID_ARG, "block origin outside the volume");
+    if (b->global_dims[d] >= (1ll << 24)) return fail(INR_ERR_UNSUPPORTED, "global dims must be < 2^24");
+  }
+  return INR_OK;
+}
+
+// N_l = floor(N_min * b^l) in double (R3); S_l = min(T, (N_l+1)^3) (R2).
+static void build_net(const inr_config& c, NetDesc& net) {
+  memset(&net, 0, sizeof net);
+  net.L = c.levels;
+  net.F = c.features;
+  net.H = c.mlp_hidden_layers;
+  net.LF = c.levels * c.features;
+  net.D = c.out_dim;
+  net.bias = c.mlp_bias ? 1 : 0;
+  uint64_t T = 1ull << c.log2_table_size;
+  net.table_mask = (uint32_t)(T - 1);
+  int64_t off = 0;
+  for (int l = 0; l < c.levels; ++l) {
+    double r = std::floor((double)c.base_resolution * std::pow((double)c.per_level_scale, (double)l));
+    uint64_t res = (uint64_t)r;
+    double dense = std::pow((double)res + 1.0, 3.0);
+    LevelInfo& lv = net.lv[l];
+    lv.res = (uint32_t)res;
+    if (dense <= (double)T) { lv.size = (uint32_t)((res + 1) * (res + 1) * (res + 1)); lv.dense = 1; }
+    else { lv.size = (uint32_t)T; lv.dense = 0; }
+    lv.offset = off;
+    off += (int64_t)lv.size * c.features;
+  }
+  for (int k = 0; k <= net.H; ++k) {
+    net.in_dim[k] = k == 0 ? net.LF : kWidth;
+    net.out_dim[k] = k == net.H ? net.D : kWidth;
+    net.w_off[k] = off;
+    off += (int64_t)net.in_dim[k] * net.out_dim[k];
+    net.b_off[k] = -1;
+    if (net.bias) { net.b_off[k] = off; off += net.out_dim[k]; }
+  }
+  net.nparams = off;
+}
+
+static void philox_key(uint64_t seed, uint32_t stream, uint32_t& k0, uint32_t& k1) {
+  k0 = (uint32_t)(seed & 0xffffffffu);
+  k1 = (uint32_t)(seed >> 32) ^ stream;
+}
+
+static void block_geometry(inr_model* m) {
+  const inr_block& b = m->blk;
+  int64_t B[3], c[3];
+  for (int d = 0; d < 3; ++d) { B[d] = (b.global_dims[d] + b.n[d] - 1) / b.n[d]; c[d] = b.origin[d] / b.n[d]; }
+  m->block_id = (uint32_t)((c[2] * B[1] + c[1]) * B[0] + c[0]);
+  m->nfaces = 0;
+  for (int d = 0; d < 3; ++d) {
+    if (b.origin[d] > 0) m->faces[m->nfaces++] = 2 * d;
+    if (b.origin[d] + b.n[d] < b.global_dims[d]) m->faces[m->nfaces++] = 2 * d + 1;
+  }
+}
+
+// frozen: parameters only; host_only: no device parameter buffer (staged lazily on decode).
+static inr_status alloc_model(inr_model* m, bool frozen, bool host_only = false) {
+  m->P = m->net.nparams;
+  m->P_pad = (m->P + 63) / 64 * 64;
+  size_t bytes = (size_t)m->P_pad * sizeof(float) * (host_only ? 0 : (frozen ? 1 : 4)) + 256;
+  if (!frozen && m->cfg.reduction == INR_REDUCE_DETERMINISTIC) bytes += (size_t)m->P_pad * 8;
+  CK(cudaMalloc(&m->mem, bytes));
+  char* p = (char*)m->mem;
+  if (!host_only) { m->params = (float*)p; p += m->P_pad * 4; }
+  if (!frozen) {
+    m->grads = (float*)p; p += m->P_pad * 4;
+    m->adam_m = (float*)p; p += m->P_pad * 4;
+    m->adam_v = (float*)p; p += m->P_pad * 4;
+    if (m->cfg.reduction == INR_REDUCE_DETERMINISTIC) { m->gfx = (unsigned long long*)p; p += m->P_pad * 8; }
+  }
+  m->step_total = (long long*)p;
+  m->step_cur = (long long*)(p + 8);
+  m->acc = (double*)(p + 16);
+  m->flag = (int*)(p + 48);
+  CK(cudaMemset(p, 0, 256));
+  return INR_OK;
+}
+
+static inr_status init_state(inr_model* m, uint64_t seed, cudaStream_t st) {
+  uint32_t k0, k1;
+  philox_key(seed, 0, k0, k1);
+  launch_init_params(m->net, m->params, k0, k1, m->block_id, st);
+  CK_LAUNCH("init_params");
+  size_t n = (size_t)m->P_pad * 4;
+  CK(cudaMemsetAsync(m->grads, 0, n * 3, st));  // grads, m, v are contiguous
+  if (m->gfx) CK(cudaMemsetAsync(m->gfx, 0, (size_t)m->P_pad * 8, st));
+  char* tail = (char*)m->step_total;
+  CK(cudaMemsetAsync(tail, 0, 256, st));
+  m->steps = 0;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_create(const inr_config* cfg, const inr_block* block, int device, inr_model** out) {
+  if (!out) return fail(INR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  inr_status s = validate_config(cfg);
+  if (s) return s;
+  if ((s = validate_block(block))) return s;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(INR_ERR_INVALID_ARG, "device %d out of range", device);
+  CK(cudaSetDevice(device));
+  inr_model* m = new inr_model();
+  m->cfg = *cfg;
+  m->blk = *block;
+  m->device = device;
+  build_net(*cfg, m->net);
+  block_geometry(m);
+  if ((s = alloc_model(m, false)) || (s = init_state(m, cfg->seed, 0))) {
+    if (m->mem) cudaFree(m->mem);
+    delete m;
+    return s;
+  }
+  CK(cudaStreamSynchronize(0));
+  *out = m;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_reset(inr_model* m, uint64_t seed) {
+  if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
+  if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
+  CK(cudaSetDevice(m->device));
+  m->cfg.seed = seed;
+  inr_status s = init_state(m, seed, 0);
+  if (s) return s;
+  CK(cudaStreamSynchronize(0));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_destroy(inr_model* m) {
+  if (!m) return INR_OK;
+  cudaSetDevice(m->device);
+  if (m->host_resident && m->params) cudaFree(m->params);
+  if (m->mem) cudaFree(m->mem);
+  if (m->host_params) cudaFreeHost(m->host_params);
+  delete m;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_param_count(const inr_model* m, int64_t* count) {
+  if (!m || !count) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *count = m->P;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_param_bytes(const inr_model* m, int64_t* bytes) {
+  if (!m || !bytes) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *bytes = m->P * (int64_t)sizeof(float);
+  return INR_OK;
+}
+
+extern "C" inr_status inr_steps(const inr_model* m, int64_t* steps) {
+  if (!m || !steps) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *steps = m->steps;
+  return INR_OK;
+}
+
+extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
+  if (!o) return;
+  o->lambda = 0.5f;
+  o->boundary_batch = 0;
+  o->lr0 = 1e-2f;
+  o->lr_decay = 0.8f;
+  o->lr_step = 500;
+  o->beta1 = 0.9f;
+  o->beta2 = 0.999f;
+  o->eps = 1e-8f;
+  o->vmin = 0.f;
+  o->vmax = 1.f;
+  o->target_psnr = 0.f;
+  o->check_interval = 0;
+}
+
+// Make sure device-resident parameters exist for a (possibly host-resident) model.
+static inr_status ensure_device_params(const inr_model* cm, cudaStream_t st) {
+  inr_model* m = const_cast<inr_model*>(cm);
+  if (!m->host_resident || m->staged) return INR_OK;
+  if (!m->params) CK(cudaMalloc((void**)&m->params, (size_t)m->P_pad * 4));
+  CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P * 4, cudaMemcpyHostToDevice, st));
+  m->staged = true;
+  return INR_OK;
+}
+
+static ModelDev model_dev(const inr_model* m) {
+  ModelDev d;
+  memset(&d, 0, sizeof d);
+  d.params = m->params;
+  d.grads = m->grads;
+  d.adam_m = m->adam_m;
+  d.adam_v = m->adam_v;
+  d.grads_fx = m->gfx;
+  d.step_total = m->step_total;
+  d.step_cur = m->step_cur;
+  d.acc = m->acc;
+  d.flag = m->flag;
+  for (int k = 0; k < 3; ++k) {
+    d.o[k] = (int)m->blk.origin[k];
+    d.n[k] = m->blk.n[k];
+    d.N[k] = (int)m->blk.global_dims[k];
+  }
+  d.block_id = m->block_id;
+  d.nfaces = m->nfaces;
+  for (int k = 0; k < 6; ++k) d.faces[k] = m->faces[k];
+  d.vmin = m->vmin;
+  d.vrange = m->vmax - m->vmin;
+  d.inv_range = m->vmax > m->vmin ? (float)(1.0 / ((double)m->vmax - (double)m->vmin)) : 0.f;
+  return d;
+}
+
+static bool same_shape(const inr_config& a, const inr_config& b) {
+  // (the seed may differ: each model draws its own Philox streams)
+  return a.levels == b.levels && a.features == b.features && a.log2_table_size == b.log2_table_size &&
+         a.base_resolution == b.base_resolution && a.per_level_scale == b.per_level_scale &&
+         a.mlp_width == b.mlp_width && a.mlp_hidden_layers == b.mlp_hidden_layers && a.out_dim == b.out_dim &&
+         a.mlp_bias == b.mlp_bias && a.precision == b.precision && a.reduction == b.reduction;
+}
+
+static inr_status validate_view(const inr_model* m, const inr_view* v) {
+  if (!v || !v->base) return fail(INR_ERR_INVALID_ARG, "view is NULL");
+  for (int d = 0; d < 3; ++d) {
+    int64_t need_lo = m->blk.origin[d];
+    int64_t need_hi = std::min<int64_t>(m->blk.origin[d] + m->blk.n[d], m->blk.global_dims[d] - 1);
+    if (v->lo[d] > need_lo || v->lo[d] + v->dims[d] - 1 < need_hi)
+      return fail(INR_ERR_INVALID_ARG, "view does not cover nodes [o, min(o+n, N-1)] on axis %d", d);
+  }
+  return INR_OK;
+}
+
+static inr_status fit_impl(inr_model* const* models, const inr_view* views, int32_t nmodels, int32_t steps,
+                           int32_t batch, const inr_fit_opts* opts, inr_fit_report* out, cudaStream_t st) {
+  if (!models || !views || nmodels < 1) return fail(INR_ERR_INVALID_ARG, "models/views missing");
+  if (!opts) return fail(INR_ERR_INVALID_ARG, "opts is NULL");
+  if (steps < 1) return fail(INR_ERR_INVALID_ARG, "steps must be >= 1");
+  if (batch < 1) return fail(INR_ERR_INVALID_ARG, "batch must be >= 1");
+  if (!(opts->lambda >= 0.f && opts->lambda <= 1.f)) return fail(INR_ERR_INVALID_ARG, "lambda must be in [0,1]");
+  if (opts->boundary_batch < 0) return fail(INR_ERR_INVALID_ARG, "boundary_batch must be >= 0");
+  if (opts->lr_step < 1) return fail(INR_ERR_INVALID_ARG, "lr_step must be >= 1");
+  if (!(opts->vmax >= opts->vmin)) return fail(INR_ERR_INVALID_ARG, "vmax < vmin");
+  for (int i = 0; i < nmodels; ++i) {
+    if (!models[i]) return fail(INR_ERR_INVALID_ARG, "model %d is NULL", i);
+    if (models[i]->frozen) return fail(INR_ERR_STATE, "model %d is a frozen cache snapshot", i);
+    if (models[i]->device != models[0]->device || !same_shape(models[i]->cfg, models[0]->cfg))
+      return fail(INR_ERR_INVALID_ARG, "all models of a group must share device and config");
+    inr_status s = validate_view(models[i], &views[i]);
+    if (s) return s;
+  }
+  const inr_model* m0 = models[0];
+  CK(cudaSetDevice(m0->device));
+  const bool tc = m0->cfg.precision == INR_PREC_FP16_MLP;
+  if (tc && !tc_supported(m0->net)) return fail(INR_ERR_UNSUPPORTED, "configuration not supported by the tcgen05 MLP");
+
+  FitScalars fs;
+  fs.B_u = batch;
+  fs.B_b = opts->boundary_batch;
+  fs.lambda = opts->lambda;
+  fs.det = m0->cfg.reduction == INR_REDUCE_DETERMINISTIC;
+  AdamScalars as;
+  as.lr0 = opts->lr0;
+  as.lr_decay = opts->lr_decay;
+  as.lr_step = opts->lr_step;
+  as.beta1 = opts->beta1;
+  as.beta2 = opts->beta2;
+  as.eps = opts->eps;
+
+  for (int i = 0; i < nmodels; ++i) {
+    models[i]->vmin = opts->vmin;
+    models[i]->vmax = opts->vmax;
+  }
+  const int nchunks = (nmodels + kMaxGroup - 1) / kMaxGroup;
+  std::vector<GroupArgs> groups(nchunks);
+  for (int c = 0; c < nchunks; ++c) {
+    GroupArgs& g = groups[c];
+    memset(&g, 0, sizeof g);
+    g.net = m0->net;
+    g.nmodels = std::min(kMaxGroup, nmodels - c * kMaxGroup);
+    for (int j = 0; j < g.nmodels; ++j) {
+      const inr_model* m = models[c * kMaxGroup + j];
+      const inr_view& v = views[c * kMaxGroup + j];
+      ModelDev& d = g.md[j];
+      d = model_dev(m);
+      d.vbase = v.base;
+      uint32_t k0;
+      philox_key(m->cfg.seed, 1, d.k0, d.k1u);
+      philox_key(m->cfg.seed, 2, k0, d.k1b);
+      for (int k = 0; k < 3; ++k) { d.vlo[k] = v.lo[k]; d.vstride[k] = v.stride[k]; }
+    }
+  }
+  auto enqueue_step = [&](cudaStream_t s) {
+    for (int c = 0; c < nchunks; ++c) {
+      launch_step_begin(groups[c], groups[c].nmodels, s);
+      if (tc) launch_fit_tc(groups[c], groups[c].nmodels, fs, s);
+      else launch_fit_simt(groups[c], groups[c].nmodels, fs, s);
+      launch_adam(groups[c], groups[c].nmodels, as, s);
+    }
+  };
+  const bool probing = out && opts->target_psnr > 0.f && opts->check_interval > 0;
+  const int launches_per_step = 3 * nchunks;
+  // Replay a captured step when there are enough steps to amortize capture and
+  // the stream is capturable (not the legacy default stream).
+  cudaGraphExec_t exec = nullptr;
+  if (steps >= 4 && st != nullptr) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    long long before = g_launches.load();
+    enqueue_step(st);
+    g_launches.store(before);  // captured launches are counted per replay below
+    cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  }
+  int taken = 0;
+  bool reached_all = false;
+  std::vector<double> psnr(nmodels, 0.0);
+  std::vector<int> reached(nmodels, 0);
+  for (int s = 0; s < steps; ++s) {
+    if (exec) {
+      cudaError_t e = cudaGraphLaunch(exec, st);
+      if (e != cudaSuccess) { cudaGraphExecDestroy(exec); return cuda_fail(e, "cudaGraphLaunch"); }
+      count_launch(launches_per_step);
+    } else {
+      enqueue_step(st);
+      CK_LAUNCH("fit step");
+    }
+    taken = s + 1;
+    if (probing && taken % opts->check_interval == 0) {
+      for (int c = 0; c < nchunks; ++c)
+        for (int j = 0; j < groups[c].nmodels; ++j)
+          CK(cudaMemsetAsync(groups[c].md[j].acc + 2, 0, sizeof(double), st));
+      for (int c = 0; c < nchunks; ++c) launch_probe(groups[c], groups[c].nmodels, st);
+      CK_LAUNCH("probe");
+      CK(cudaStreamSynchronize(st));
+      reached_all = true;
+      for (int i = 0; i < nmodels; ++i) {
+        double sse = 0;
+        CK(cudaMemcpy(&sse, models[i]->acc + 2, sizeof sse, cudaMemcpyDeviceToHost));
+        double mse = sse / 32768.0;
+        psnr[i] = mse <= 0 ? 200.0 : std::min(200.0, -10.0 * std::log10(mse));
+        reached[i] = psnr[i] >= opts->target_psnr;
+        reached_all &= reached[i] != 0;
+      }
+      if (reached_all) break;
+    }
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  for (int i = 0; i < nmodels; ++i) models[i]->steps += taken;
+  if (!out) return INR_OK;
+  CK(cudaStreamSynchronize(st));
+  bool nonfinite = false;
+  for (int i = 0; i < nmodels; ++i) {
+    const inr_model* m = models[i];
+    double acc[2];
+    int flag = 0;
+    CK(cudaMemcpy(acc, m->acc, sizeof acc, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&flag, m->flag, sizeof flag, cudaMemcpyDeviceToHost));
+    inr_fit_report& r = out[i];
+    r.steps_taken = taken;
+    r.reached_target = reached[i];
+    r.constant_field = opts->vmax == opts->vmin;
+    int bb = m->nfaces > 0 ? opts->boundary_batch : 0;
+    r.loss_uniform = acc[0] / (double)batch;
+    r.loss_boundary = bb > 0 ? acc[1] / (double)bb : 0.0;
+    r.probe_psnr = psnr[i];
+    if (flag || !std::isfinite(r.loss_uniform) || !std::isfinite(r.loss_boundary)) nonfinite = true;
+  }
+  if (nonfinite) return fail(INR_ERR_NONFINITE, "non-finite loss or parameter after %d steps", taken);
+  if (opts->vmax == opts->vmin) g_err = "warning: constant field (vmax == vmin), targets are 0";
+  return INR_OK;
+}
+
+extern "C" inr_status inr_fit(inr_model* m, const inr_view* v, int32_t steps, int32_t batch,
+                              const inr_fit_opts* opts, inr_fit_report* out, cudaStream_t st) {
+  if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
+  return fit_impl(&m, v, 1, steps, batch, opts, out, st);
+}
+
+extern "C" inr_status inr_fit_group(inr_model* const* models, const inr_view* views, int32_t nmodels,
+                                    int32_t steps, int32_t batch, const inr_fit_opts* opts, inr_fit_report* out,
+                                    cudaStream_t st) {
+  return fit_impl(models, views, nmodels, steps, batch, opts, out, st);
+}
+
+// ------------------------------------------------------------------ decode
+extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
+                                      const int64_t* out_stride, const float* ref, double* sse_dev,
+                                      cudaStream_t st) {
+  if (!m || !res || !out) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  for (int d = 0; d < 3; ++d)
+    if (res[d] < 1 || res[d] > (1 << 20)) return fail(INR_ERR_INVALID_ARG, "res must be in 1..2^20");
+  if (ref && !sse_dev) return fail(INR_ERR_INVALID_ARG, "ref given without sse_dev");
+  CK(cudaSetDevice(m->device));
+  inr_status s = ensure_device_params(m, st);
+  if (s) return s;
+  long long os[3];
+  if (out_stride) { for (int d = 0; d < 3; ++d) os[d] = out_stride[d]; }
+  else { os[0] = 1; os[1] = res[0]; os[2] = (long long)res[0] * res[1]; }
+  int r[3] = {res[0], res[1], res[2]};
+  ModelDev md = model_dev(m);
+  launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
+  CK_LAUNCH("decode_grid");
+  return INR_OK;
+}
+
+static inr_status decode_group_impl(const inr_model* const* models, int32_t nmodels, const float* xyz, int64_t q,
+                                    float* out, int32_t strict, cudaStream_t st) {
+  if (!models || nmodels < 1 || (q > 0 && (!xyz || !out))) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (q < 0) return fail(INR_ERR_INVALID_ARG, "q must be >= 0");
+  if (nmodels > kMaxGroup) return fail(INR_ERR_UNSUPPORTED, "at most %d models per decode group", kMaxGroup);
+  const inr_model* m0 = models[0];
+  if (!m0) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
+  CK(cudaSetDevice(m0->device));
+  QueryArgs* qa = new QueryArgs();
+  memset(qa, 0, sizeof *qa);
+  qa->net = m0->net;
+  long long nb = 1;
+  for (int d = 0; d < 3; ++d) {
+    qa->n[d] = m0->blk.n[d];
+    qa->N[d] = (int)m0->blk.global_dims[d];
+    qa->B[d] = (int)((m0->blk.global_dims[d] + m0->blk.n[d] - 1) / m0->blk.n[d]);
+    nb *= qa->B[d];
+  }
+  if (nb > kMaxRouteBlocks) { delete qa; return fail(INR_ERR_UNSUPPORTED, "at most %d blocks in a volume", kMaxRouteBlocks); }
+  qa->nblocks = (int)nb;
+  for (long long b = 0; b < nb; ++b) qa->slot_of_block[b] = -1;
+  for (int i = 0; i < nmodels; ++i) {
+    const inr_model* m = models[i];
+    if (!m || !same_shape(m->cfg, m0->cfg) || m->device != m0->device) {
+      delete qa;
+      return fail(INR_ERR_INVALID_ARG, "decode group models must share config and device");
+    }
+    for (int d = 0; d < 3; ++d)
+      if (m->blk.n[d] != m0->blk.n[d] || m->blk.global_dims[d] != m0->blk.global_dims[d]) {
+        delete qa;
+        return fail(INR_ERR_INVALID_ARG, "decode group models must tile one volume");
+      }
+    inr_status s = ensure_device_params(m, st);
+    if (s) { delete qa; return s; }
+    qa->md[i] = model_dev(m);
+    qa->slot_of_block[m->block_id] = (int16_t)i;
+  }
+  int* dflag = nullptr;
+  if (strict) {
+    cudaError_t e = cudaMallocAsync((void**)&dflag, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int), st);
+    if (e != cudaSuccess) { delete qa; return cuda_fail(e, "strict flag"); }
+  }
+  if (q > 0) launch_decode_query_simt(*qa, xyz, q, out, dflag, st);
+  delete qa;
+  CK_LAUNCH("decode_query");
+  if (strict) {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, dflag, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFreeAsync(dflag, st);
+    if (h) return fail(INR_ERR_DOMAIN, "a query coordinate lies outside the global domain");
+  }
+  return INR_OK;
+}
+
+extern "C" inr_status inr_decode(const inr_model* m, const float* xyz, int64_t q, float* out, int32_t strict,
+                                 cudaStream_t st) {
+  if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
+  return decode_group_impl(&m, 1, xyz, q, out, strict, st);
+}
+
+extern "C" inr_status inr_decode_group(const inr_model* const* models, int32_t nmodels, const float* xyz, int64_t q,
+                                       float* out, int32_t strict, cudaStream_t st) {
+  return decode_group_impl(models, nmodels, xyz, q, out, strict, st);
+}
+
+extern "C" inr_status inr_value_range(const inr_view* v, float* minmax, cudaStream_t st) {
+  if (!v || !v->base || !minmax) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  for (int d = 0; d < 3; ++d)
+    if (v->dims[d] < 1) return fail(INR_ERR_INVALID_ARG, "view dims must be >= 1");
+  int dims[3] = {v->dims[0], v->dims[1], v->dims[2]};
+  long long s[3] = {v->stride[0], v->stride[1], v->stride[2]};
+  launch_range(v->base, dims, s, minmax, st);
+  CK_LAUNCH("value_range");
+  return INR_OK;
+}
+
+// ------------------------------------------------------------ parity surface
+static inr_status copy_out(const inr_model* m, const float* src, float* host, int64_t n) {
+  if (!m || !host) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (n != m->P) return fail(INR_ERR_INVALID_ARG, "n must equal inr_param_count (%lld)", (long long)m->P);
+  if (!src) return fail(INR_ERR_STATE, "this state does not exist on a frozen snapshot");
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(host, src, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_get_params(const inr_model* m, float* host, int64_t n) {
+  if (m && m->host_resident && !m->staged) {
+    if (!host || n != m->P) return fail(INR_ERR_INVALID_ARG, "bad arguments");
+    memcpy(host, m->host_params, (size_t)n * 4);
+    return INR_OK;
+  }
+  return copy_out(m, m ? m->params : nullptr, host, n);
+}
+extern "C" inr_status inr_get_grads(const inr_model* m, float* host, int64_t n) {
+  return copy_out(m, m ? m->grads : nullptr, host, n);
+}
+extern "C" inr_status inr_get_adam_state(const inr_model* m, float* mh, float* vh, int64_t n) {
+  inr_status s = copy_out(m, m ? m->adam_m : nullptr, mh, n);
+  if (s) return s;
+  return copy_out(m, m->adam_v, vh, n);
+}
+extern "C" inr_status inr_set_params(inr_model* m, const float* host, int64_t n) {
+  if (!m || !host) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
+  if (n != m->P) return fail(INR_ERR_INVALID_ARG, "n must equal inr_param_count (%lld)", (long long)m->P);
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(m->params, host, (size_t)n * 4, cudaMemcpyHostToDevice));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_t q, uint32_t* idx, float* feat,
+                                       cudaStream_t st) {
+  if (!m || (q > 0 && !x01)) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (q <= 0) return INR_OK;
+  CK(cudaSetDevice(m->device));
+  inr_status s = ensure_device_params(m, st);
+  if (s) return s;
+  launch_debug_encode(m->net, m->params, x01, q, idx, feat, st);
+  CK_LAUNCH("debug_encode");
+  return INR_OK;
+}
+
+extern "C" inr_status inr_debug_forward(const inr_model* m, const float* x01, int64_t q, float* y, cudaStream_t st) {
+  if (!m || (q > 0 && (!x01 || !y))) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (q <= 0) return INR_OK;
+  CK(cudaSetDevice(m->device));
+  inr_status s = ensure_device_params(m, st);
+  if (s) return s;
+  if (m->cfg.precision == INR_PREC_FP16_MLP) launch_debug_forward_tc(m->net, m->params, x01, q, y, st);
+  else launch_debug_forward_simt(m->net, m->params, x01, q, y, st);
+  CK_LAUNCH("debug_forward");
+  return INR_OK;
+}
+
+// ------------------------------------------------------------------ cache
+struct CacheSlot {
+  int64_t timestep;
+  std::vector<inr_model*> models;
+  std::vector<const inr_model*> cmodels;
+};
+
+struct inr_cache {
+  int capacity;
+  bool host_resident;
+  int device;
+  std::deque<CacheSlot> slots;
+  int64_t bytes = 0;
+};
+
+static void free_slot(inr_cache* c, CacheSlot& s) {
+  for (inr_model* m : s.models) {
+    c->bytes -= m->P * 4;
+    inr_destroy(m);
+  }
+  s.models.clear();
+}
+
+extern "C" inr_status cache_create(int32_t capacity, int32_t host_resident, int device, inr_cache** out) {
+  if (!out) return fail(INR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (capacity < 1) return fail(INR_ERR_INVALID_ARG, "capacity must be >= 1");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(INR_ERR_INVALID_ARG, "device %d out of range", device);
+  inr_cache* c = new inr_cache();
+  c->capacity = capacity;
+  c->host_resident = host_resident != 0;
+  c->device = device;
+  *out = c;
+  return INR_OK;
+}
+
+extern "C" inr_status cache_destroy(inr_cache* c) {
+  if (!c) return INR_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& s : c->slots) free_slot(c, s);
+  delete c;
+  return INR_OK;
+}
+
+extern "C" inr_status cache_evict(inr_cache* c, int64_t* evicted) {
+  if (!c) return fail(INR_ERR_INVALID_ARG, "cache is NULL");
+  if (c->slots.empty()) return fail(INR_ERR_STATE, "evict on an empty cache");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());  // snapshots may still be read by queued decodes
+  if (evicted) *evicted = c->slots.front().timestep;
+  free_slot(c, c->slots.front());
+  c->slots.pop_front();
+  return INR_OK;
+}
+
+extern "C" inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* const* blocks, int32_t nblocks,
+                                   int64_t* evicted, cudaStream_t st) {
+  if (!c || !blocks || nblocks < 1) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (!c->slots.empty() && timestep <= c->slots.back().timestep)
+    return fail(INR_ERR_INVALID_ARG, "timesteps must be strictly increasing (last %lld)",
+                (long long)c->slots.back().timestep);
+  for (int i = 0; i < nblocks; ++i)
+    if (!blocks[i] || blocks[i]->device != c->device) return fail(INR_ERR_INVALID_ARG, "block %d invalid", i);
+  if (evicted) *evicted = -1;
+  CK(cudaSetDevice(c->device));
+  if ((int)c->slots.size() == c->capacity) {
+    inr_status s = cache_evict(c, evicted);
+    if (s) return s;
+  }
+  CacheSlot slot;
+  slot.timestep = timestep;
+  for (int i = 0; i < nblocks; ++i) {
+    const inr_model* src = blocks[i];
+    inr_model* m = new inr_model();
+    m->cfg = src->cfg;
+    m->blk = src->blk;
+    m->device = src->device;
+    m->net = src->net;
+    m->block_id = src->block_id;
+    m->nfaces = src->nfaces;
+    memcpy(m->faces, src->faces, sizeof m->faces);
+    m->vmin = src->vmin;
+    m->vmax = src->vmax;
+    m->steps = src->steps;
+    m->frozen = true;
+    inr_status s = alloc_model(m, true, c->host_resident);
+    if (s) { delete m; for (auto* x : slot.models) inr_destroy(x); return s; }
+    if (c->host_resident) {
+      // "the learned neural network parameters are cached in system RAM"
+      cudaError_t e = cudaMallocHost((void**)&m->host_params, (size_t)m->P * 4);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(m->host_params, src->params, (size_t)m->P * 4, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2H"); }
+      m->host_resident = true;
+      m->staged = false;
+    } else {
+      cudaError_t e = cudaMemcpyAsync(m->params, src->params, (size_t)m->P * 4, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2D"); }
+    }
+    c->bytes += m->P * 4;
+    slot.models.push_back(m);
+    slot.cmodels.push_back(m);
+  }
+  if (c->host_resident) CK(cudaStreamSynchronize(st));
+  c->slots.push_back(std::move(slot));
+  return INR_OK;
+}
+
+extern "C" inr_status cache_size(const inr_cache* c, int32_t* n) {
+  if (!c || !n) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *n = (int32_t)c->slots.size();
+  return INR_OK;
+}
+
+extern "C" inr_status cache_bytes(const inr_cache* c, int64_t* bytes) {
+  if (!c || !bytes) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *bytes = c->bytes;
+  return INR_OK;
+}
+
+extern "C" inr_status cache_get(const inr_cache* c, int32_t i, int64_t* timestep, const inr_model* const** blocks,
+                                int32_t* nblocks) {
+  if (!c) return fail(INR_ERR_INVALID_ARG, "cache is NULL");
+  if (i < 0 || i >= (int)c->slots.size()) return fail(INR_ERR_INVALID_ARG, "slot %d out of range", i);
+  const CacheSlot& s = c->slots[i];
+  if (timestep) *timestep = s.timestep;
+  if (blocks) *blocks = s.cmodels.data();
+  if (nblocks) *nblocks = (int32_t)s.cmodels.size();
+  return INR_OK;
+}

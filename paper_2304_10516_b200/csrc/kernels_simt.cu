@@ -1,0 +1,572 @@
+// kernels_simt.cu — fp32 CUDA-core kernels of libinr (sm_100a):
+//   * parameter init (R14), step bookkeeping, the fused fp32 fit step
+//     (sample -> target -> encode -> MLP fwd -> Eq. 2 -> MLP bwd -> scatter),
+//     the PyTorch-form Adam (R12), decode (grid / query), probe PSNR,
+//     value range, debug encode/forward.
+// The fp32 fit kernel is the parity mode (INR_PREC_FP32); the tensor-core fit
+// kernel for INR_PREC_FP16_MLP lives in kernels_tc.cu and shares the sampler,
+// encode and scatter code of common.cuh.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace inr {
+
+constexpr int kTile = 64;        // samples per CTA (one per thread) in the SIMT kernels
+constexpr int kLd = kTile + 1;   // smem row stride (bank-conflict-free column access)
+
+// ----------------------------------------------------------------- init
+// value_j = fl32(lo + (hi - lo) * U_j) in fp64 with each op rounded, U_j =
+// u01(Philox(key(seed, 0), (j, block_id, 0, 0)).x) (R14).
+__global__ void init_params_kernel(NetDesc net, float* __restrict__ params, uint32_t k0, uint32_t k1,
+                                   uint32_t block_id) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < net.nparams;
+       j += (long long)gridDim.x * blockDim.x) {
+    double a = -1.0;  // -1: zero (bias)
+    if (j < net.w_off[0]) {
+      a = 1e-4;
+    } else {
+      for (int k = 0; k <= net.H; ++k) {
+        long long w0 = net.w_off[k], w1 = w0 + (long long)net.in_dim[k] * net.out_dim[k];
+        if (j >= w0 && j < w1) { a = sqrt(6.0 / (double)net.in_dim[k]); break; }
+      }
+    }
+    float v = 0.f;
+    if (a > 0) {
+      U4 u = philox((uint32_t)j, block_id, 0u, 0u, k0, k1);
+      double U = (double)(u.x >> 8) * 5.9604644775390625e-08;
+      double lo = -a, hi = a;
+      v = __double2float_rn(__dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), U)));
+    }
+    params[j] = v;
+  }
+}
+
+// --------------------------------------------------------- step bookkeeping
+// Zero this step's gradient accumulators and loss sums; step_cur <- step_total++.
+__global__ void step_begin_kernel(GroupArgs g) {
+  const ModelDev& md = g.md[blockIdx.y];
+  long long n = g.net.nparams;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long s = *md.step_total;
+    *md.step_cur = s;
+    *md.step_total = s + 1;
+    md.acc[0] = 0.0;
+    md.acc[1] = 0.0;
+  }
+  long long stride = (long long)gridDim.x * blockDim.x;
+  long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (md.grads_fx) {
+    for (long long i = i0; i < n; i += stride) md.grads_fx[i] = 0ull;
+  } else {
+    float4* g4 = reinterpret_cast<float4*>(md.grads);
+    for (long long i = i0; i < n / 4; i += stride) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long i = (n / 4) * 4 + i0; i < n; i += stride) md.grads[i] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------ SIMT MLP fwd
+// act: smem rows of kLd floats; rows [0, LF) hold the features of the tile;
+// rows LF + 64 k + n hold the pre-activation z_k[n] of hidden layer k.
+// Returns y (D = 1).  h_{k+1} = max(z_k, 0).
+__device__ float mlp_forward_simt(const NetDesc& net, const float* __restrict__ P, float* act, int t) {
+  const float* hin = act;
+  int in = net.LF;
+  bool relu = false;
+  for (int k = 0; k < net.H; ++k) {
+    const float* W = P + net.w_off[k];
+    float* z = act + (size_t)(net.LF + kWidth * k) * kLd;
+    for (int n = 0; n < kWidth; ++n) {
+      float acc = net.bias ? __ldg(P + net.b_off[k] + n) : 0.f;
+      const float* Wr = W + (size_t)n * in;
+      for (int i = 0; i < in; ++i) {
+        float h = hin[i * kLd + t];
+        if (relu) h = fmaxf(h, 0.f);
+        acc = fmaf(__ldg(Wr + i), h, acc);
+      }
+      z[n * kLd + t] = acc;
+    }
+    hin = z;
+    in = kWidth;
+    relu = true;
+  }
+  const float* W = P + net.w_off[net.H];
+  float acc = net.bias ? __ldg(P + net.b_off[net.H]) : 0.f;
+  for (int i = 0; i < in; ++i) {
+    float h = hin[i * kLd + t];
+    if (relu) h = fmaxf(h, 0.f);
+    acc = fmaf(__ldg(W + i), h, acc);
+  }
+  return acc;
+}
+
+template <int F>
+__device__ __forceinline__ void encode_to_smem(const NetDesc& net, const float* __restrict__ P, const float x[3],
+                                               float* act, int t) {
+  for (int l = 0; l < net.L; ++l) {
+    float f[F];
+    encode_level<F>(P, net.lv[l], net.table_mask, x, f);
+#pragma unroll
+    for (int j = 0; j < F; ++j) act[(l * F + j) * kLd + t] = f[j];
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// --------------------------------------------------------- fused fit (fp32)
+// One CTA = kTile samples of one model; blockIdx.y = model.  Sample i < B_u is
+// uniform, B_u <= i < B_u + B_b boundary (B_b = 0 for blocks without interior
+// faces, lambda' = 0 then [R11]).  The per-tile MLP weight gradient is summed in
+// sample order inside the CTA and added once per tile (atomic or exact int64).
+template <int F>
+__global__ void __launch_bounds__(kTile) fit_simt_kernel(GroupArgs g, FitScalars fs) {
+  extern __shared__ float smem[];
+  const NetDesc& net = g.net;
+  const ModelDev& md = g.md[blockIdx.y];
+  const int t = threadIdx.x;
+  const int B_b = md.nfaces > 0 ? fs.B_b : 0;
+  const int total = fs.B_u + B_b;
+  const int i = blockIdx.x * kTile + t;
+  if (blockIdx.x * kTile >= total) return;
+  const bool valid = i < total;
+  const float* __restrict__ P = md.params;
+  float* __restrict__ G = md.grads;
+  unsigned long long* __restrict__ GX = md.grads_fx;
+
+  float* act = smem;                                   // (LF + 64 H) rows
+  float* dzA = act + (size_t)(net.LF + kWidth * net.H) * kLd;
+  float* dzB = dzA + (size_t)kWidth * kLd;
+  __shared__ double red[2][kTile / 32];
+
+  const uint32_t step = (uint32_t)*md.step_cur;
+  float x[3] = {0.f, 0.f, 0.f};
+  float target = 0.f;
+  if (valid) {
+    draw_sample(md, i, fs.B_u, step, x);
+    target = sample_target(md, x);
+  }
+  encode_to_smem<F>(net, P, x, act, t);
+  // No barrier needed: every thread only touches its own smem column until the
+  // per-tile weight-gradient reduction below.
+  float y = mlp_forward_simt(net, P, act, t);
+
+  // Eq. 2: dL/dy = (1 - lambda') sgn(y - t) / B_u  (uniform)  or  lambda' sgn / B_b.
+  float lam = B_b > 0 ? fs.lambda : 0.f;
+  bool is_b = i >= fs.B_u;
+  float d = y - target;
+  float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
+  float dy = is_b ? lam * sg / (float)max(B_b, 1) : (1.f - lam) * sg / (float)fs.B_u;
+  {
+    double au = (valid && !is_b) ? fabs((double)d) : 0.0;
+    double ab = (valid && is_b) ? fabs((double)d) : 0.0;
+    au = warp_sum(au);
+    ab = warp_sum(ab);
+    if ((t & 31) == 0) { red[0][t >> 5] = au; red[1][t >> 5] = ab; }
+  }
+
+  // ---- backward through the output layer (D = 1)
+  const int H = net.H;
+  const float* hH = act + (size_t)(net.LF + kWidth * (H - 1)) * kLd;   // z_{H-1}
+  {
+    const float* Wo = P + net.w_off[H];
+    for (int n = 0; n < kWidth; ++n) {
+      float z = hH[n * kLd + t];
+      dzA[n * kLd + t] = z > 0.f ? __ldg(Wo + n) * dy : 0.f;          // dz_{H-1}
+    }
+  }
+  __shared__ float dys[kTile];
+  dys[t] = dy;
+  __syncthreads();
+  if (t == 0) {
+    double su = 0, sb = 0;
+    for (int w = 0; w < kTile / 32; ++w) { su += red[0][w]; sb += red[1][w]; }
+    if (su != 0.0) atomicAdd(md.acc + 0, su);
+    if (sb != 0.0) atomicAdd(md.acc + 1, sb);
+  }
+  // dW_H[0][n] = sum_s dy_s relu(z_{H-1}[n][s]); db_H = sum_s dy_s  (thread n owns entry n)
+  {
+    float acc = 0.f;
+    for (int s = 0; s < kTile; ++s) acc = fmaf(dys[s], fmaxf(hH[t * kLd + s], 0.f), acc);
+    if (acc != 0.f) grad_add(G, GX, net.w_off[H] + t, acc);
+    if (net.bias && t == 0) {
+      float b = 0.f;
+      for (int s = 0; s < kTile; ++s) b += dys[s];
+      if (b != 0.f) grad_add(G, GX, net.b_off[H], b);
+    }
+  }
+  // ---- hidden layers k = H-1 .. 0:  z_k = W_k h_k + b_k
+  float* dz = dzA;
+  float* dzn = dzB;
+  float dfeat[64];
+  for (int k = H - 1; k >= 0; --k) {
+    const int in = net.in_dim[k];
+    const float* hk = k == 0 ? act : act + (size_t)(net.LF + kWidth * (k - 1)) * kLd;
+    const bool relu = k > 0;
+    // weight gradient of layer k: entry e = n*in + ii, summed over the tile in sample order
+    for (int e = t; e < kWidth * in; e += kTile) {
+      int n = e / in, ii = e - n * in;
+      float acc = 0.f;
+      for (int s = 0; s < kTile; ++s) {
+        float h = hk[ii * kLd + s];
+        if (relu) h = fmaxf(h, 0.f);
+        acc = fmaf(dz[n * kLd + s], h, acc);
+      }
+      if (acc != 0.f) grad_add(G, GX, net.w_off[k] + e, acc);
+    }
+    if (net.bias) {
+      float acc = 0.f;
+      for (int s = 0; s < kTile; ++s) acc += dz[t * kLd + s];
+      if (acc != 0.f) grad_add(G, GX, net.b_off[k] + t, acc);
+    }
+    // dh_k = W_k^T dz_k for this thread's sample; dz_{k-1} = dh_k * 1[z_{k-1} > 0]
+    const float* W = P + net.w_off[k];
+    if (k > 0) {
+      const float* zprev = act + (size_t)(net.LF + kWidth * (k - 1)) * kLd;
+      for (int ii = 0; ii < in; ++ii) {
+        float acc = 0.f;
+        for (int n = 0; n < kWidth; ++n) acc = fmaf(__ldg(W + (size_t)n * in + ii), dz[n * kLd + t], acc);
+        dzn[ii * kLd + t] = zprev[ii * kLd + t] > 0.f ? acc : 0.f;
+      }
+      __syncthreads();
+      float* tmp = dz; dz = dzn; dzn = tmp;
+    } else {
+      for (int ii = 0; ii < in; ++ii) {
+        float acc = 0.f;
+        for (int n = 0; n < kWidth; ++n) acc = fmaf(__ldg(W + (size_t)n * in + ii), dz[n * kLd + t], acc);
+        dfeat[ii] = acc;
+      }
+    }
+  }
+  // ---- table scatter-add
+  if (valid) {
+    for (int l = 0; l < net.L; ++l) {
+      float df[F];
+#pragma unroll
+      for (int j = 0; j < F; ++j) df[j] = dfeat[l * F + j];
+      scatter_level<F>(G, GX, net.lv[l], net.table_mask, x, df);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- Adam
+// PyTorch torch.optim.Adam (R12): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// p -= (lr/bc1) m / (sqrt(v)/sqrt(bc2) + eps); lr = lr0 decay^floor(s/lr_step) (R13).
+// Deterministic mode converts the exact int64 sums to fp32 first.
+__global__ void adam_kernel(GroupArgs g, AdamScalars as) {
+  const ModelDev& md = g.md[blockIdx.y];
+  const long long n = g.net.nparams;
+  const long long s = *md.step_cur;
+  const double lr = (double)as.lr0 * pow((double)as.lr_decay, (double)(s / as.lr_step));
+  const double bc1 = 1.0 - pow((double)as.beta1, (double)(s + 1));
+  const double bc2 = 1.0 - pow((double)as.beta2, (double)(s + 1));
+  const float step_size = (float)(lr / bc1);
+  const float inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  const float b1 = as.beta1, b2 = as.beta2, eps = as.eps;
+  const float ob1 = 1.f - b1, ob2 = 1.f - b2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  bool bad = false;
+  float* __restrict__ P = md.params;
+  float* __restrict__ G = md.grads;
+  float* __restrict__ M = md.adam_m;
+  float* __restrict__ V = md.adam_v;
+  if (md.grads_fx) {
+    const float sc = 1.f / (float)(1ll << kFixedShift);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+      float gi = (float)((double)(long long)md.grads_fx[i] * (double)sc);
+      G[i] = gi;
+      float m = fmaf(b1, M[i], ob1 * gi), v = fmaf(b2, V[i], ob2 * gi * gi);
+      float p = P[i] - step_size * m / (sqrtf(v) * inv_sqrt_bc2 + eps);
+      M[i] = m; V[i] = v; P[i] = p;
+      bad |= !isfinite(p);
+    }
+  } else {
+    const long long n4 = n / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+      float4 gg = reinterpret_cast<const float4*>(G)[i];
+      float4 mm = reinterpret_cast<float4*>(M)[i];
+      float4 vv = reinterpret_cast<float4*>(V)[i];
+      float4 pp = reinterpret_cast<float4*>(P)[i];
+#define ADAM1(c)                                                              \
+  mm.c = fmaf(b1, mm.c, ob1 * gg.c);                                          \
+  vv.c = fmaf(b2, vv.c, ob2 * gg.c * gg.c);                                   \
+  pp.c = pp.c - step_size * mm.c / (sqrtf(vv.c) * inv_sqrt_bc2 + eps);        \
+  bad |= !isfinite(pp.c);
+      ADAM1(x) ADAM1(y) ADAM1(z) ADAM1(w)
+#undef ADAM1
+      reinterpret_cast<float4*>(M)[i] = mm;
+      reinterpret_cast<float4*>(V)[i] = vv;
+      reinterpret_cast<float4*>(P)[i] = pp;
+    }
+    for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+      float gi = G[i];
+      float m = fmaf(b1, M[i], ob1 * gi), v = fmaf(b2, V[i], ob2 * gi * gi);
+      float p = P[i] - step_size * m / (sqrtf(v) * inv_sqrt_bc2 + eps);
+      M[i] = m; V[i] = v; P[i] = p;
+      bad |= !isfinite(p);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(md.flag, 1);
+}
+
+// ------------------------------------------------------------- decode grid
+// x_j = fl32(j / R) per axis (R19); v = y (vmax - vmin) + vmin; optional SSE
+// in normalized units against ref (R18).
+template <int F>
+__global__ void __launch_bounds__(kTile) decode_grid_simt_kernel(NetDesc net, ModelDev md, int rx, int ry, int rz,
+                                                                 float* __restrict__ out, long long os0,
+                                                                 long long os1, long long os2,
+                                                                 const float* __restrict__ ref,
+                                                                 double* __restrict__ sse) {
+  extern __shared__ float smem[];
+  const int t = threadIdx.x;
+  const long long total = (long long)rx * ry * rz;
+  const long long j = blockIdx.x * (long long)kTile + t;
+  const bool valid = j < total;
+  int jx = 0, jy = 0, jz = 0;
+  if (valid) {
+    jx = (int)(j % rx);
+    long long r = j / rx;
+    jy = (int)(r % ry);
+    jz = (int)(r / ry);
+  }
+  float x[3] = {__fdiv_rn((float)jx, (float)rx), __fdiv_rn((float)jy, (float)ry), __fdiv_rn((float)jz, (float)rz)};
+  encode_to_smem<F>(net, md.params, x, smem, t);
+  float y = mlp_forward_simt(net, md.params, smem, t);
+  double e = 0.0;
+  if (valid) {
+    long long off = jx * os0 + jy * os1 + jz * os2;
+    float v = fmaf(y, md.vrange, md.vmin);
+    out[off] = v;
+    if (ref) {
+      double dd = ((double)v - (double)__ldg(ref + off)) / (double)md.vrange;
+      e = dd * dd;
+    }
+  }
+  if (sse) {
+    e = warp_sum(e);
+    if ((t & 31) == 0 && e != 0.0) atomicAdd(sse, e);
+  }
+}
+
+// ------------------------------------------------------------ decode query
+// Route p to block min(max(floor(p/n),0),B-1) (R5); x = fl32(fl32(p - o) / n).
+template <int F>
+__global__ void __launch_bounds__(kTile) decode_query_simt_kernel(QueryArgs qa, const float* __restrict__ xyz,
+                                                                  long long q, float* __restrict__ out,
+                                                                  int* __restrict__ domain_flag) {
+  extern __shared__ float smem[];
+  const int t = threadIdx.x;
+  const long long j = blockIdx.x * (long long)kTile + t;
+  const bool valid = j < q;
+  float p[3] = {0.f, 0.f, 0.f};
+  if (valid) {
+    p[0] = __ldg(xyz + 3 * j); p[1] = __ldg(xyz + 3 * j + 1); p[2] = __ldg(xyz + 3 * j + 2);
+  }
+  int bc[3];
+  bool outside = false;
+  for (int d = 0; d < 3; ++d) {
+    outside |= !(p[d] >= 0.f && p[d] <= (float)(qa.N[d] - 1));
+    int b = (int)floorf(__fdiv_rn(p[d], (float)qa.n[d]));
+    bc[d] = min(max(b, 0), qa.B[d] - 1);
+  }
+  int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
+  int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
+  const ModelDev& md = qa.md[slot < 0 ? 0 : slot];
+  float x[3];
+  for (int d = 0; d < 3; ++d) x[d] = __fdiv_rn(__fsub_rn(p[d], (float)md.o[d]), (float)md.n[d]);
+  encode_to_smem<F>(qa.net, md.params, x, smem, t);
+  float y = mlp_forward_simt(qa.net, md.params, smem, t);
+  if (valid) {
+    out[j] = slot < 0 ? __int_as_float(0x7fc00000) : fmaf(y, md.vrange, md.vmin);
+    if (outside && domain_flag) atomicOr(domain_flag, 1);
+  }
+}
+
+// -------------------------------------------------------------- probe PSNR
+// SSE of Phi against sampler targets on the 32^3 cell-centred probe lattice
+// x = (j + 0.5)/32, accumulated into md.acc[2].
+template <int F>
+__global__ void __launch_bounds__(kTile) probe_simt_kernel(GroupArgs g) {
+  extern __shared__ float smem[];
+  const ModelDev& md = g.md[blockIdx.y];
+  const int t = threadIdx.x;
+  const int j = blockIdx.x * kTile + t;  // < 32768
+  float x[3] = {((j & 31) + 0.5f) / 32.f, (((j >> 5) & 31) + 0.5f) / 32.f, ((j >> 10) + 0.5f) / 32.f};
+  float tgt = sample_target(md, x);
+  encode_to_smem<F>(g.net, md.params, x, smem, t);
+  float y = mlp_forward_simt(g.net, md.params, smem, t);
+  double e = (double)(y - tgt) * (double)(y - tgt);
+  e = warp_sum(e);
+  if ((t & 31) == 0) atomicAdd(md.acc + 2, e);
+}
+
+// ------------------------------------------------------------ value range
+__device__ __forceinline__ void atomic_min_f(float* a, float v) {
+  if (v >= 0.f) atomicMin(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMax(reinterpret_cast<unsigned int*>(a), __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_max_f(float* a, float v) {
+  if (v >= 0.f) atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMin(reinterpret_cast<unsigned int*>(a), __float_as_uint(v));
+}
+
+__global__ void range_kernel(const float* __restrict__ base, int dx, int dy, int dz, long long s0, long long s1,
+                             long long s2, float* __restrict__ minmax) {
+  float lo = __int_as_float(0x7f800000), hi = -lo;
+  const long long total = (long long)dx * dy * dz;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total;
+       j += (long long)gridDim.x * blockDim.x) {
+    int ix = (int)(j % dx);
+    long long r = j / dx;
+    int iy = (int)(r % dy), iz = (int)(r / dy);
+    float v = __ldg(base + ix * s0 + iy * s1 + iz * s2);
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_min_f(minmax, lo);
+    atomic_max_f(minmax + 1, hi);
+  }
+}
+
+// ----------------------------------------------------------- debug encode
+template <int F>
+__global__ void debug_encode_kernel(NetDesc net, const float* __restrict__ P, const float* __restrict__ x01,
+                                    long long q, uint32_t* __restrict__ idx, float* __restrict__ feat) {
+  long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  float x[3] = {__ldg(x01 + 3 * j), __ldg(x01 + 3 * j + 1), __ldg(x01 + 3 * j + 2)};
+  for (int l = 0; l < net.L; ++l) {
+    if (idx) {
+      Cell c = level_cell(x, net.lv[l].res);
+      for (int k = 0; k < 8; ++k) idx[(j * net.L + l) * 8 + k] = corner_index(c, k, net.lv[l], net.table_mask);
+    }
+    if (feat) {
+      float f[F];
+      encode_level<F>(P, net.lv[l], net.table_mask, x, f);
+      for (int k = 0; k < F; ++k) feat[j * net.LF + l * F + k] = f[k];
+    }
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(kTile) debug_forward_simt_kernel(NetDesc net, const float* __restrict__ P,
+                                                                   const float* __restrict__ x01, long long q,
+                                                                   float* __restrict__ y) {
+  extern __shared__ float smem[];
+  const int t = threadIdx.x;
+  long long j = blockIdx.x * (long long)kTile + t;
+  float x[3] = {0.f, 0.f, 0.f};
+  if (j < q) { x[0] = __ldg(x01 + 3 * j); x[1] = __ldg(x01 + 3 * j + 1); x[2] = __ldg(x01 + 3 * j + 2); }
+  encode_to_smem<F>(net, P, x, smem, t);
+  float v = mlp_forward_simt(net, P, smem, t);
+  if (j < q) y[j] = v;
+}
+
+// ============================================================ host launchers
+static size_t simt_fwd_smem(const NetDesc& net) { return (size_t)(net.LF + kWidth * net.H) * kLd * sizeof(float); }
+static size_t simt_fit_smem(const NetDesc& net) { return simt_fwd_smem(net) + 2 * (size_t)kWidth * kLd * sizeof(float); }
+
+#define DISPATCH_F(F_, ...)                              \
+  switch (F_) {                                          \
+    case 1: { constexpr int FF = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int FF = 2; __VA_ARGS__; } break; \
+    case 4: { constexpr int FF = 4; __VA_ARGS__; } break; \
+    case 8: { constexpr int FF = 8; __VA_ARGS__; } break; \
+    default: break;                                      \
+  }
+
+template <typename K>
+static void set_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t k1, uint32_t block_id,
+                        cudaStream_t st) {
+  int blocks = (int)std::min<long long>((net.nparams + 255) / 256, 148 * 16);
+  init_params_kernel<<<blocks, 256, 0, st>>>(net, params, k0, k1, block_id);
+  count_launch();
+}
+
+void launch_step_begin(const GroupArgs& g, int nmodels, cudaStream_t st) {
+  int bx = (int)std::min<long long>((g.net.nparams / 4 + 255) / 256, 148 * 4 / max(1, nmodels) + 1);
+  step_begin_kernel<<<dim3(max(bx, 1), nmodels), 256, 0, st>>>(g);
+  count_launch();
+}
+
+void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st) {
+  int total = fs.B_u + fs.B_b;
+  dim3 grid((total + kTile - 1) / kTile, nmodels);
+  size_t sm = simt_fit_smem(g.net);
+  DISPATCH_F(g.net.F, set_smem(fit_simt_kernel<FF>, sm); fit_simt_kernel<FF><<<grid, kTile, sm, st>>>(g, fs));
+  count_launch();
+}
+
+void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st) {
+  long long per = (g.net.nparams / 4 + 255) / 256;
+  int bx = (int)std::max<long long>(1, std::min<long long>(per, (148 * 8 + nmodels - 1) / nmodels));
+  adam_kernel<<<dim3(bx, nmodels), 256, 0, st>>>(g, as);
+  count_launch();
+}
+
+void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st) {
+  size_t sm = simt_fwd_smem(g.net);
+  DISPATCH_F(g.net.F, set_smem(probe_simt_kernel<FF>, sm);
+             probe_simt_kernel<FF><<<dim3(32768 / kTile, nmodels), kTile, sm, st>>>(g));
+  count_launch();
+}
+
+void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+                             const long long os[3], const float* ref, double* sse, cudaStream_t st) {
+  long long total = (long long)res[0] * res[1] * res[2];
+  size_t sm = simt_fwd_smem(net);
+  unsigned grid = (unsigned)((total + kTile - 1) / kTile);
+  DISPATCH_F(net.F, set_smem(decode_grid_simt_kernel<FF>, sm);
+             decode_grid_simt_kernel<FF><<<grid, kTile, sm, st>>>(net, md, res[0], res[1], res[2], out, os[0], os[1],
+                                                                  os[2], ref, sse));
+  count_launch();
+}
+
+void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag,
+                              cudaStream_t st) {
+  size_t sm = simt_fwd_smem(qa.net);
+  unsigned grid = (unsigned)((q + kTile - 1) / kTile);
+  DISPATCH_F(qa.net.F, set_smem(decode_query_simt_kernel<FF>, sm);
+             decode_query_simt_kernel<FF><<<grid, kTile, sm, st>>>(qa, xyz, q, out, dflag));
+  count_launch();
+}
+
+void launch_range(const float* base, const int dims[3], const long long s[3], float* minmax, cudaStream_t st) {
+  long long total = (long long)dims[0] * dims[1] * dims[2];
+  int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 8));
+  range_kernel<<<blocks, 256, 0, st>>>(base, dims[0], dims[1], dims[2], s[0], s[1], s[2], minmax);
+  count_launch();
+}
+
+void launch_debug_encode(const NetDesc& net, const float* P, const float* x01, long long q, uint32_t* idx,
+                         float* feat, cudaStream_t st) {
+  unsigned grid = (unsigned)((q + 127) / 128);
+  DISPATCH_F(net.F, debug_encode_kernel<FF><<<grid, 128, 0, st>>>(net, P, x01, q, idx, feat));
+  count_launch();
+}
+
+void launch_debug_forward_simt(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
+                               cudaStream_t st) {
+  size_t sm = simt_fwd_smem(net);
+  unsigned grid = (unsigned)((q + kTile - 1) / kTile);
+  DISPATCH_F(net.F, set_smem(debug_forward_simt_kernel<FF>, sm);
+             debug_forward_simt_kernel<FF><<<grid, kTile, sm, st>>>(net, P, x01, q, y));
+  count_launch();
+}
+
+}  // namespace inr

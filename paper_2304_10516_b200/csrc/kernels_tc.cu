@@ -1,0 +1,643 @@
+// kernels_tc.cu — the fused fit step with the MLP on 5th-generation tensor
+// cores (tcgen05.mma, kind::f16: fp16 operands in shared memory, fp32
+// accumulators in TMEM), INR_PREC_FP16_MLP (R17).
+//
+// One CTA = 4 warps = 128 threads; a tile is 128 samples, sample t <-> thread t
+// <-> TMEM lane t.  Per tile:
+//   sampler + encode (CUDA cores, common.cuh) -> fp16 feature tile h_0 in smem
+//   forward  z_k = h_k W_k^T   : M=128, N=64,   K=in_k   (A K-major, B K-major)
+//   epilogue (TMEM -> regs): + b_k, ReLU, fp16 -> h_{k+1} tile; last hidden
+//            layer feeds the 64->1 output layer on CUDA cores (fp32), Eq. 2
+//   backward dW_k += dz_k^T h_k : M=64,  N=in_k+8, K=128 (A MN-major, B MN-major;
+//            the +8 columns hold a constant 1 so column in_k accumulates db_k)
+//            dh_k = dz_k W_k     : M=128, N=in_k,   K=64  (A K-major, B MN-major)
+//   table scatter-add of dfeat (CUDA cores, common.cuh)
+// dW_k stays in TMEM across all tiles a CTA processes and is flushed once.
+// dz is scaled by 2^s (loss scaling, exact) so fp16 keeps its precision.
+//
+// Shared-memory operand tiles use the canonical SWIZZLE_NONE ("interleaved")
+// layout: 8 rows x 16 B core matrices; element (row r, col c) of a tile with
+// C columns sits at byte  (r%8)*16 + (r/8)*SBO + (c/8)*128 + (c%8)*2,
+// SBO = (C/8)*128.  Read with (row = M/N dim, col = K dim) it is the K-major
+// layout (LBO = 128, SBO); read with (row = K dim, col = M/N dim) it is the
+// MN-major layout (SBO' = 128, LBO' = SBO).  So every tile serves both GEMMs
+// that need it without a transposed copy.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace inr {
+
+namespace tc {
+
+constexpr int kThreads = 128;
+constexpr int kTileM = 128;
+
+struct Layout {
+  uint32_t w[kMaxLayers];        // fp16 W_k tile [64 x in_k] (k < H)
+  uint32_t w_sbo[kMaxLayers];
+  uint32_t h[kMaxLayers];        // fp16 h_k tile [128 x (in_k + ones)] (k < H), h_0 = features
+  uint32_t h_sbo[kMaxLayers];
+  uint32_t dz, dz_sbo;           // fp16 dz tile [128 x 64]
+  uint32_t bias;                 // fp32 [H][64]
+  uint32_t wout;                 // fp32 W_H[64], then b_H
+  uint32_t red;                  // fp32 dW_H[64], db_H, pad
+  uint32_t mbar;                 // 8 B
+  uint32_t tslot;                // 4 B: TMEM base address
+  uint32_t bytes;                // dynamic smem requested
+  uint32_t col_dw[kMaxLayers];   // TMEM column of the dW_k accumulator
+  uint32_t ncols;                // TMEM columns allocated (power of 2)
+  int ones;                      // 8 if biases (ones group appended), else 0
+  int ctas_per_sm;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
+  return d;
+}
+
+// kind::f16 instruction descriptor: fp16 A/B, fp32 D.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// 16 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Row r of a canonical tile: write 8 consecutive columns [8j, 8j+8) as fp16.
+__device__ __forceinline__ void st_row8(uint8_t* tile, uint32_t sbo, int r, int j, const float* v) {
+  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
+  __half2 h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
+  uint4 u;
+  u.x = *reinterpret_cast<uint32_t*>(&h0);
+  u.y = *reinterpret_cast<uint32_t*>(&h1);
+  u.z = *reinterpret_cast<uint32_t*>(&h2);
+  u.w = *reinterpret_cast<uint32_t*>(&h3);
+  *reinterpret_cast<uint4*>(tile + (r & 7) * 16 + (r >> 3) * sbo + j * 128) = u;
+}
+
+__device__ __forceinline__ uint32_t tile_off(uint32_t sbo, int r, int c) {
+  return (r & 7) * 16 + (r >> 3) * sbo + (c >> 3) * 128 + (c & 7) * 2;
+}
+
+// Sum 64 per-lane values over the warp; lane l ends with the column sums of
+// columns c0 = 32 b4 + 16 b3 + 8 b2 + 4 b1 + 2 b0 and c0 + 1 (b = lane bits).
+__device__ __forceinline__ void warp_transpose_reduce64(float* v, int lane) {
+#pragma unroll
+  for (int half = 32, off = 16; off >= 1; half >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      float keep = up ? v[j + half] : v[j];
+      float send = up ? v[j] : v[j + half];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+// Issue the K loop of one GEMM (single thread).  a/b: start addresses; the
+// per-K-step (16 elements) advance of each operand is given explicitly.
+__device__ __forceinline__ void gemm(uint32_t tmem_d, uint32_t a, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_step,
+                                     uint32_t b, uint32_t b_lbo, uint32_t b_sbo, uint32_t b_step, int ksteps,
+                                     uint32_t idesc, bool accum_first) {
+  for (int k = 0; k < ksteps; ++k) {
+    uint64_t ad = make_desc(a + k * a_step, a_lbo, a_sbo);
+    uint64_t bd = make_desc(b + k * b_step, b_lbo, b_sbo);
+    mma_f16(tmem_d, ad, bd, idesc, (k > 0 || accum_first) ? 1u : 0u);
+  }
+}
+
+template <int F>
+__global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitScalars fs, Layout lay,
+                                                            float loss_scale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const NetDesc& net = g.net;
+  const ModelDev& md = g.md[blockIdx.y];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int H = net.H, LF = net.LF, ones = lay.ones;
+  const int B_b = md.nfaces > 0 ? fs.B_b : 0;
+  const int total = fs.B_u + B_b;
+  const int ntiles = (total + kTileM - 1) / kTileM;
+  const float* __restrict__ P = md.params;
+  float* __restrict__ G = md.grads;
+  unsigned long long* __restrict__ GX = md.grads_fx;
+  const float inv_scale = 1.f / loss_scale;
+
+  float* bias = reinterpret_cast<float*>(smem + lay.bias);
+  float* wout = reinterpret_cast<float*>(smem + lay.wout);
+  float* red = reinterpret_cast<float*>(smem + lay.red);
+  const uint32_t mbar = smem_u32(smem + lay.mbar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
+
+  // ---- setup: TMEM allocation, barrier, weights -> fp16 tiles, constants
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(lay.ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (t == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int k = 0; k < H; ++k) {
+    const int in = net.in_dim[k];
+    const float* W = P + net.w_off[k];
+    for (int e = t; e < 64 * in; e += kThreads) {
+      int n = e / in, i = e - n * in;
+      *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) = __float2half_rn(W[e]);
+    }
+    for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
+    if (ones) {  // constant ones group of h_k: column in_k = 1, in_k+1..+7 = 0
+      uint4 u = make_uint4(0x3C00u, 0u, 0u, 0u);  // half(1.0) in the low half of the first word
+      *reinterpret_cast<uint4*>(smem + lay.h[k] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[k] + (in >> 3) * 128) = u;
+    }
+  }
+  for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
+  if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
+  for (int i = t; i < 66; i += kThreads) red[i] = 0.f;
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  uint32_t phase = 0;
+  bool first = true;
+  const uint32_t step = (uint32_t)*md.step_cur;
+  const float lam = B_b > 0 ? fs.lambda : 0.f;
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int i = tile * kTileM + t;
+    const bool valid = i < total;
+    const bool is_b = i >= fs.B_u;
+    float x[3] = {0.f, 0.f, 0.f};
+    float target = 0.f;
+    if (valid) {
+      draw_sample(md, i, fs.B_u, step, x);
+      target = sample_target(md, x);
+    }
+    // ---- encode -> fp16 h_0 row
+    {
+      float f[64];
+#pragma unroll
+      for (int l = 0; l < kMaxLevels; ++l) {
+        if (l < net.L) {
+          float fl[F];
+          encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+#pragma unroll
+          for (int j = 0; j < F; ++j)
+            if (l * F + j < 64) f[l * F + j] = fl[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j * 8 < LF) st_row8(smem + lay.h[0], lay.h_sbo[0], t, j, f + 8 * j);
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+
+    // ---- forward through the hidden layers
+    uint32_t mask[kMaxLayers][2];
+    float hH[64];
+    for (int k = 0; k < H; ++k) {
+      const int in = net.in_dim[k];
+      if (t == 0) {
+        fence_after();
+        gemm(tmem, smem_u32(smem + lay.h[k]), 128, lay.h_sbo[k], 256, smem_u32(smem + lay.w[k]), 128,
+             lay.w_sbo[k], 256, in / 16, make_idesc(128, 64, 0, 0), false);
+        mma_commit(mbar);
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1;
+      fence_after();
+      float z[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_base + c * 16, z + c * 16);
+      tmem_wait_ld();
+      uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+      for (int n = 0; n < 64; ++n) {
+        float v = z[n] + bias[k * 64 + n];
+        bool pos = v > 0.f;
+        if (n < 32) m0 |= (uint32_t)pos << n; else m1 |= (uint32_t)pos << (n - 32);
+        z[n] = pos ? v : 0.f;
+      }
+      mask[k][0] = m0;
+      mask[k][1] = m1;
+      if (k + 1 < H) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, j, z + 8 * j);
+      } else {
+#pragma unroll
+        for (int n = 0; n < 64; ++n) hH[n] = z[n];
+      }
+      fence_async_smem();
+      fence_before();
+      __syncthreads();
+    }
+    // ---- output layer (fp32, CUDA cores) and Eq. 2
+    float y = wout[64];
+#pragma unroll
+    for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
+    const float d = y - target;
+    const float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
+    const float dy = is_b ? lam * sg / (float)max(B_b, 1) : (1.f - lam) * sg / (float)fs.B_u;
+    {
+      double au = (valid && !is_b) ? fabs((double)d) : 0.0;
+      double ab = (valid && is_b) ? fabs((double)d) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        au += __shfl_xor_sync(0xffffffffu, au, o);
+        ab += __shfl_xor_sync(0xffffffffu, ab, o);
+      }
+      if (lane == 0) {
+        if (au != 0.0) atomicAdd(md.acc + 0, au);
+        if (ab != 0.0) atomicAdd(md.acc + 1, ab);
+      }
+    }
+    // dW_H[n] = sum_s dy_s h_H[s][n], db_H = sum_s dy_s (warp transpose-reduce, then smem)
+    {
+      float v[64];
+#pragma unroll
+      for (int n = 0; n < 64; ++n) v[n] = dy * hH[n];
+      warp_transpose_reduce64(v, lane);
+      int c0 = ((lane >> 4) & 1) * 32 + ((lane >> 3) & 1) * 16 + ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 +
+               (lane & 1) * 2;
+      atomicAdd(red + c0, v[0]);
+      atomicAdd(red + c0 + 1, v[1]);
+      float s = dy;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) atomicAdd(red + 64, s);
+    }
+    // dz_{H-1} = dy W_H * 1[z_{H-1} > 0], scaled by 2^s
+    {
+      float dz[64];
+      const float sdy = dy * loss_scale;
+#pragma unroll
+      for (int n = 0; n < 64; ++n) {
+        bool pos = ((n < 32 ? mask[H - 1][0] >> n : mask[H - 1][1] >> (n - 32)) & 1u) != 0;
+        dz[n] = pos ? sdy * wout[n] : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, t, j, dz + 8 * j);
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+
+    // ---- backward through the hidden layers
+    float dfeat[64];
+    for (int k = H - 1; k >= 0; --k) {
+      const int in = net.in_dim[k];
+      if (t == 0) {
+        fence_after();
+        // dW_k (+ db_k in column in_k): A = dz^T (MN-major), B = h_k (MN-major), K = 128 samples
+        gemm(tmem + lay.col_dw[k], smem_u32(smem + lay.dz), lay.dz_sbo, 128, 2 * lay.dz_sbo,
+             smem_u32(smem + lay.h[k]), lay.h_sbo[k], 128, 2 * lay.h_sbo[k], kTileM / 16,
+             make_idesc(64, in + ones, 1, 1), !first);
+        // dh_k = dz_k W_k: A = dz (K-major, K = 64 outputs), B = W_k (MN-major, N = in_k)
+        gemm(tmem, smem_u32(smem + lay.dz), 128, lay.dz_sbo, 256, smem_u32(smem + lay.w[k]), lay.w_sbo[k], 128,
+             2 * lay.w_sbo[k], 64 / 16, make_idesc(128, in, 0, 1), false);
+        mma_commit(mbar);
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1;
+      fence_after();
+      float dh[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c * 16 < in) tmem_ld16(tmem + lane_base + c * 16, dh + c * 16);
+      tmem_wait_ld();
+      if (k > 0) {
+#pragma unroll
+        for (int n = 0; n < 64; ++n) {
+          bool pos = ((n < 32 ? mask[k - 1][0] >> n : mask[k - 1][1] >> (n - 32)) & 1u) != 0;
+          dh[n] = pos ? dh[n] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, t, j, dh + 8 * j);
+      } else {
+#pragma unroll
+        for (int n = 0; n < 64; ++n) dfeat[n] = dh[n] * inv_scale;
+      }
+      fence_async_smem();
+      fence_before();
+      __syncthreads();
+    }
+    first = false;
+    // ---- table scatter-add
+    if (valid) {
+#pragma unroll
+      for (int l = 0; l < kMaxLevels; ++l) {
+        if (l < net.L) {
+          float df[F];
+#pragma unroll
+          for (int j = 0; j < F; ++j) df[j] = (l * F + j < 64) ? dfeat[l * F + j] : 0.f;
+          scatter_level<F>(G, GX, net.lv[l], net.table_mask, x, df);
+        }
+      }
+    }
+  }
+
+  // ---- flush the CTA's weight gradients (TMEM dW_k, smem dW_H) once
+  if (!first) {
+    fence_after();
+    for (int k = 0; k < H; ++k) {
+      const int in = net.in_dim[k];
+      const int ncol = in + ones;
+      // M = 64 accumulator: row 16w + r lives in lane 32w + r (r < 16)
+      for (int c = 0; c < ncol; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_base + lay.col_dw[k] + c, v);
+        tmem_wait_ld();
+        if (lane < 16) {
+          const int n = warp * 16 + lane;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            int col = c + j;
+            float gval = v[j] * inv_scale;
+            if (col < in) grad_add(G, GX, net.w_off[k] + (size_t)n * in + col, gval);
+            else if (col == in && ones) grad_add(G, GX, net.b_off[k] + n, gval);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (!first) {
+    for (int n = t; n < 64; n += kThreads) grad_add(G, GX, net.w_off[H] + n, red[n]);
+    if (t == 0 && net.bias) grad_add(G, GX, net.b_off[H], red[64]);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(lay.ncols));
+}
+
+// ============================================================ host side
+static bool build_layout(const NetDesc& net, Layout& L) {
+  memset(&L, 0, sizeof L);
+  if (net.LF % 16 != 0 || net.LF > 64 || net.H < 1 || net.H > kMaxLayers - 1 || net.D != 1) return false;
+  L.ones = net.bias ? 8 : 0;
+  uint32_t off = 0;
+  auto take = [&](uint32_t bytes, uint32_t align) {
+    off = (off + align - 1) / align * align;
+    uint32_t o = off;
+    off += bytes;
+    return o;
+  };
+  for (int k = 0; k < net.H; ++k) {
+    int in = net.in_dim[k];
+    L.w_sbo[k] = (uint32_t)(in / 8) * 128;
+    L.w[k] = take(64 * in * 2, 1024);
+    L.h_sbo[k] = (uint32_t)((in + L.ones) / 8) * 128;
+    L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
+  }
+  L.dz_sbo = 8 * 128;
+  L.dz = take(kTileM * 64 * 2, 1024);
+  L.bias = take(net.H * 64 * 4, 16);
+  L.wout = take(65 * 4, 16);
+  L.red = take(66 * 4, 16);
+  L.mbar = take(8, 8);
+  L.tslot = take(4, 4);
+  // TMEM: [0, 64) layer accumulator; then dW_k (M = 64 rows, in_k + ones columns)
+  // (8-column granularity; the last region is padded so 16-column loads stay inside)
+  uint32_t col = 64;
+  for (int k = 0; k < net.H; ++k) {
+    L.col_dw[k] = col;
+    col += (uint32_t)(net.in_dim[k] + L.ones);
+  }
+  col = std::max(col, L.col_dw[net.H - 1] + (uint32_t)((net.in_dim[net.H - 1] + L.ones + 15) / 16 * 16));
+  if (col > 512) return false;
+  L.ncols = 32;
+  while (L.ncols < col) L.ncols <<= 1;
+  L.ctas_per_sm = (int)(512 / L.ncols);
+  // request enough shared memory that no more CTAs than TMEM allows share an SM
+  uint32_t need = off + 128;
+  uint32_t floor_bytes = 232448u / (uint32_t)(L.ctas_per_sm + 1) + 1024;
+  L.bytes = std::max(need, std::min<uint32_t>(floor_bytes, 232448u));
+  if (need > 232448u) return false;
+  // actual residency is then limited by both shared memory and TMEM
+  L.ctas_per_sm = std::min<int>(L.ctas_per_sm, (int)(232448u / L.bytes));
+  return L.ctas_per_sm >= 1;
+}
+
+bool tc_supported(const NetDesc& net) {
+  Layout L;
+  return build_layout(net, L);
+}
+
+static float loss_scale_for(int B_u) {
+  int e = 0;
+  while ((1 << (e + 1)) <= B_u && e < 24) ++e;
+  return (float)(1 << e);
+}
+
+void launch_fit_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st) {
+  Layout L;
+  if (!build_layout(g.net, L)) return;
+  const int total = fs.B_u + fs.B_b;
+  const int ntiles = (total + kTileM - 1) / kTileM;
+  const int slots = 148 * L.ctas_per_sm;
+  int per_model = std::max(1, std::min(ntiles, (slots + nmodels - 1) / nmodels));
+  dim3 grid(per_model, nmodels);
+  float ls = loss_scale_for(fs.B_u);
+  switch (g.net.F) {
+#define CASE_F(FF)                                                                                  \
+  case FF:                                                                                          \
+    cudaFuncSetAttribute(fit_tc_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
+    fit_tc_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls);                               \
+    break;
+    CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
+#undef CASE_F
+    default: break;
+  }
+  count_launch();
+}
+
+// ------------------------------------------------------------ forward only
+// Network output for block-normalized coordinates with the same tensor-core
+// forward as the fit kernel (debug / parity surface).
+template <int F>
+__global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, const float* __restrict__ P,
+                                                                const float* __restrict__ x01, long long q,
+                                                                float* __restrict__ yout, Layout lay) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int t = threadIdx.x, warp = t >> 5;
+  const int H = net.H, LF = net.LF;
+  float* bias = reinterpret_cast<float*>(smem + lay.bias);
+  float* wout = reinterpret_cast<float*>(smem + lay.wout);
+  const uint32_t mbar = smem_u32(smem + lay.mbar);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(lay.ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (t == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int k = 0; k < H; ++k) {
+    const int in = net.in_dim[k];
+    const float* W = P + net.w_off[k];
+    for (int e = t; e < 64 * in; e += kThreads) {
+      int n = e / in, i = e - n * in;
+      *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) = __float2half_rn(W[e]);
+    }
+    for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
+  }
+  for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
+  if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  uint32_t phase = 0;
+  const long long ntiles = (q + kTileM - 1) / kTileM;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long j = tile * kTileM + t;
+    float x[3] = {0.f, 0.f, 0.f};
+    if (j < q) { x[0] = __ldg(x01 + 3 * j); x[1] = __ldg(x01 + 3 * j + 1); x[2] = __ldg(x01 + 3 * j + 2); }
+    {
+      float f[64];
+#pragma unroll
+      for (int l = 0; l < kMaxLevels; ++l) {
+        if (l < net.L) {
+          float fl[F];
+          encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+#pragma unroll
+          for (int jj = 0; jj < F; ++jj)
+            if (l * F + jj < 64) f[l * F + jj] = fl[jj];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (jj * 8 < LF) st_row8(smem + lay.h[0], lay.h_sbo[0], t, jj, f + 8 * jj);
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    float hH[64];
+    for (int k = 0; k < H; ++k) {
+      const int in = net.in_dim[k];
+      if (t == 0) {
+        fence_after();
+        gemm(tmem, smem_u32(smem + lay.h[k]), 128, lay.h_sbo[k], 256, smem_u32(smem + lay.w[k]), 128,
+             lay.w_sbo[k], 256, in / 16, make_idesc(128, 64, 0, 0), false);
+        mma_commit(mbar);
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1;
+      fence_after();
+      float z[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_base + c * 16, z + c * 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int n = 0; n < 64; ++n) z[n] = fmaxf(z[n] + bias[k * 64 + n], 0.f);
+      if (k + 1 < H) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, jj, z + 8 * jj);
+      } else {
+#pragma unroll
+        for (int n = 0; n < 64; ++n) hH[n] = z[n];
+      }
+      fence_async_smem();
+      fence_before();
+      __syncthreads();
+    }
+    float y = wout[64];
+#pragma unroll
+    for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
+    if (j < q) yout[j] = y;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(lay.ncols));
+}
+
+void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
+                             cudaStream_t st) {
+  Layout L;
+  if (!build_layout(net, L)) return;
+  long long ntiles = (q + kTileM - 1) / kTileM;
+  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles, 148 * L.ctas_per_sm));
+  switch (net.F) {
+#define CASE_F(FF)                                                                                       \
+  case FF:                                                                                               \
+    cudaFuncSetAttribute(forward_tc_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
+    forward_tc_kernel<FF><<<grid, kThreads, L.bytes, st>>>(net, P, x01, q, y, L);                       \
+    break;
+    CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
+#undef CASE_F
+    default: break;
+  }
+  count_launch();
+}
+
+}  // namespace inr

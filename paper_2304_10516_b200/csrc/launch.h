@@ -1,0 +1,63 @@
+// launch.h — internal interface between the C-ABI runtime (inr_runtime.cu)
+// and the kernel translation units.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace inr {
+
+// Kernel-parameter block for a group of models (<= kMaxGroup) sharing one config.
+struct GroupArgs {
+  NetDesc net;
+  int nmodels;
+  ModelDev md[kMaxGroup];
+};
+
+struct FitScalars {
+  int B_u, B_b;       // uniform / boundary samples per model per step
+  float lambda;
+  int det;            // deterministic reduction
+};
+
+struct AdamScalars {
+  float lr0, lr_decay;
+  long long lr_step;
+  float beta1, beta2, eps;
+};
+
+constexpr int kMaxRouteBlocks = 4096;
+struct QueryArgs {
+  NetDesc net;
+  int n[3], N[3], B[3];
+  int nblocks;
+  ModelDev md[kMaxGroup];
+  int16_t slot_of_block[kMaxRouteBlocks];
+};
+
+void count_launch(long long n = 1);
+
+void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t k1, uint32_t block_id,
+                        cudaStream_t st);
+void launch_step_begin(const GroupArgs& g, int nmodels, cudaStream_t st);
+void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
+void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st);
+void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st);
+void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+                             const long long os[3], const float* ref, double* sse, cudaStream_t st);
+void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag,
+                              cudaStream_t st);
+void launch_range(const float* base, const int dims[3], const long long s[3], float* minmax, cudaStream_t st);
+void launch_debug_encode(const NetDesc& net, const float* P, const float* x01, long long q, uint32_t* idx,
+                         float* feat, cudaStream_t st);
+void launch_debug_forward_simt(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
+                               cudaStream_t st);
+
+// tensor-core (tcgen05) kernels — kernels_tc.cu
+bool tc_supported(const NetDesc& net);
+void launch_fit_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
+void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
+                             cudaStream_t st);
+
+}  // namespace inr

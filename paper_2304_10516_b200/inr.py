@@ -1,0 +1,288 @@
+"""Thin ctypes binding of libinr.so (include/inr.h): argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does no
+computation of its own; all work runs in the sm_100a kernels of libinr.so.
+Device buffers are passed as integer device pointers (e.g. a torch CUDA
+tensor's ``data_ptr()``), streams as integer ``cudaStream_t`` handles (e.g.
+``torch.cuda.current_stream().cuda_stream``).  A missing library raises
+ImportError: there is no CPU fallback.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libinr.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "inr.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libinr.so not built at {LIB_PATH}: run __graft_entry__.build() "
+                      "(make -C paper_2304_10516_b200); there is no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---- status codes / enums (inr.h)
+INR_OK, INR_ERR_INVALID_ARG, INR_ERR_DOMAIN, INR_ERR_NONFINITE = 0, 1, 2, 3
+INR_ERR_OOM, INR_ERR_CUDA, INR_ERR_STATE, INR_ERR_UNSUPPORTED = 4, 5, 6, 7
+INR_PREC_FP32, INR_PREC_FP16_MLP = 0, 1
+INR_REDUCE_ATOMIC, INR_REDUCE_DETERMINISTIC = 0, 1
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "DOMAIN", 3: "NONFINITE", 4: "OOM", 5: "CUDA", 6: "STATE",
+                7: "UNSUPPORTED"}
+
+
+class InrError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class inr_config(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("features", ctypes.c_int32), ("log2_table_size", ctypes.c_int32),
+                ("base_resolution", ctypes.c_int32), ("per_level_scale", ctypes.c_float),
+                ("mlp_width", ctypes.c_int32), ("mlp_hidden_layers", ctypes.c_int32), ("out_dim", ctypes.c_int32),
+                ("mlp_bias", ctypes.c_int32), ("precision", ctypes.c_int32), ("reduction", ctypes.c_int32),
+                ("seed", ctypes.c_uint64)]
+
+
+class inr_block(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_int64 * 3), ("n", ctypes.c_int32 * 3), ("global_dims", ctypes.c_int64 * 3)]
+
+
+class inr_fit_opts(ctypes.Structure):
+    _fields_ = [("lambda_", ctypes.c_float), ("boundary_batch", ctypes.c_int32), ("lr0", ctypes.c_float),
+                ("lr_decay", ctypes.c_float), ("lr_step", ctypes.c_int32), ("beta1", ctypes.c_float),
+                ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("vmin", ctypes.c_float),
+                ("vmax", ctypes.c_float), ("target_psnr", ctypes.c_float), ("check_interval", ctypes.c_int32)]
+
+
+class inr_fit_report(ctypes.Structure):
+    _fields_ = [("steps_taken", ctypes.c_int32), ("reached_target", ctypes.c_int32),
+                ("constant_field", ctypes.c_int32), ("loss_uniform", ctypes.c_double),
+                ("loss_boundary", ctypes.c_double), ("probe_psnr", ctypes.c_double)]
+
+
+class inr_view(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("lo", ctypes.c_int64 * 3), ("dims", ctypes.c_int32 * 3),
+                ("stride", ctypes.c_int64 * 3)]
+
+
+_P = ctypes.c_void_p
+_I32, _I64, _U64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_SIG = {
+    "inr_last_error": (ctypes.c_char_p, []),
+    "inr_create": (_I32, [ctypes.POINTER(inr_config), ctypes.POINTER(inr_block), ctypes.c_int, _PP]),
+    "inr_reset": (_I32, [_P, _U64]),
+    "inr_destroy": (_I32, [_P]),
+    "inr_param_count": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "inr_param_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "inr_steps": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "inr_fit_opts_default": (None, [ctypes.POINTER(inr_fit_opts)]),
+    "inr_fit": (_I32, [_P, ctypes.POINTER(inr_view), _I32, _I32, ctypes.POINTER(inr_fit_opts),
+                       ctypes.POINTER(inr_fit_report), _P]),
+    "inr_fit_group": (_I32, [_PP, ctypes.POINTER(inr_view), _I32, _I32, _I32, ctypes.POINTER(inr_fit_opts),
+                             ctypes.POINTER(inr_fit_report), _P]),
+    "inr_decode": (_I32, [_P, _P, _I64, _P, _I32, _P]),
+    "inr_decode_group": (_I32, [_PP, _I32, _P, _I64, _P, _I32, _P]),
+    "inr_decode_grid": (_I32, [_P, ctypes.POINTER(_I32), _P, ctypes.POINTER(_I64), _P, _P, _P]),
+    "inr_value_range": (_I32, [ctypes.POINTER(inr_view), _P, _P]),
+    "cache_create": (_I32, [_I32, _I32, ctypes.c_int, _PP]),
+    "cache_destroy": (_I32, [_P]),
+    "cache_insert": (_I32, [_P, _I64, _PP, _I32, ctypes.POINTER(_I64), _P]),
+    "cache_evict": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "cache_size": (_I32, [_P, ctypes.POINTER(_I32)]),
+    "cache_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "cache_get": (_I32, [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_PP), ctypes.POINTER(_I32)]),
+    "inr_get_params": (_I32, [_P, _P, _I64]),
+    "inr_set_params": (_I32, [_P, _P, _I64]),
+    "inr_get_grads": (_I32, [_P, _P, _I64]),
+    "inr_get_adam_state": (_I32, [_P, _P, _P, _I64]),
+    "inr_debug_encode": (_I32, [_P, _P, _I64, _P, _P, _P]),
+    "inr_debug_forward": (_I32, [_P, _P, _I64, _P, _P]),
+    "inr_kernel_launches": (_I64, []),
+}
+for _name, (_res, _args) in _SIG.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+lib = _lib
+
+
+def inr_last_error():
+    return _lib.inr_last_error().decode()
+
+
+def _check(status):
+    if status != INR_OK:
+        raise InrError(status, inr_last_error())
+
+
+def _ptrs(handles):
+    arr = (ctypes.c_void_p * len(handles))(*[h.value if isinstance(h, ctypes.c_void_p) else h for h in handles])
+    return ctypes.cast(arr, _PP), arr
+
+
+def make_config(levels=16, features=2, log2_table_size=19, base_resolution=4, per_level_scale=2.0, mlp_width=64,
+                mlp_hidden_layers=3, out_dim=1, mlp_bias=1, precision=INR_PREC_FP32, reduction=INR_REDUCE_ATOMIC,
+                seed=0x230410516):
+    return inr_config(levels, features, log2_table_size, base_resolution, per_level_scale, mlp_width,
+                      mlp_hidden_layers, out_dim, mlp_bias, precision, reduction, seed)
+
+
+def make_block(origin, n, global_dims):
+    return inr_block((ctypes.c_int64 * 3)(*origin), (ctypes.c_int32 * 3)(*n), (ctypes.c_int64 * 3)(*global_dims))
+
+
+def make_view(base_ptr, lo, dims, stride):
+    return inr_view(base_ptr, (ctypes.c_int64 * 3)(*lo), (ctypes.c_int32 * 3)(*dims), (ctypes.c_int64 * 3)(*stride))
+
+
+def inr_fit_opts_default():
+    o = inr_fit_opts()
+    _lib.inr_fit_opts_default(ctypes.byref(o))
+    return o
+
+
+# ---- models
+def inr_create(cfg, block, device=0):
+    h = ctypes.c_void_p()
+    _check(_lib.inr_create(ctypes.byref(cfg), ctypes.byref(block), device, ctypes.byref(h)))
+    return h
+
+
+def inr_reset(m, seed):
+    _check(_lib.inr_reset(m, seed))
+
+
+def inr_destroy(m):
+    _check(_lib.inr_destroy(m))
+
+
+def inr_param_count(m):
+    n = _I64()
+    _check(_lib.inr_param_count(m, ctypes.byref(n)))
+    return n.value
+
+
+def inr_param_bytes(m):
+    n = _I64()
+    _check(_lib.inr_param_bytes(m, ctypes.byref(n)))
+    return n.value
+
+
+def inr_steps(m):
+    n = _I64()
+    _check(_lib.inr_steps(m, ctypes.byref(n)))
+    return n.value
+
+
+def inr_fit(m, view, steps, batch, opts, stream=0, report=True):
+    rep = inr_fit_report() if report else None
+    _check(_lib.inr_fit(m, ctypes.byref(view), steps, batch, ctypes.byref(opts),
+                        ctypes.byref(rep) if rep is not None else None, stream))
+    return rep
+
+
+def inr_fit_group(models, views, steps, batch, opts, stream=0, report=True):
+    pp, keep = _ptrs(models)
+    va = (inr_view * len(views))(*views)
+    reps = (inr_fit_report * len(models))() if report else None
+    _check(_lib.inr_fit_group(pp, va, len(models), steps, batch, ctypes.byref(opts), reps, stream))
+    return list(reps) if reps is not None else None
+
+
+def inr_decode(m, xyz_ptr, q, out_ptr, strict=0, stream=0):
+    _check(_lib.inr_decode(m, xyz_ptr, q, out_ptr, strict, stream))
+
+
+def inr_decode_group(models, xyz_ptr, q, out_ptr, strict=0, stream=0):
+    pp, keep = _ptrs(models)
+    _check(_lib.inr_decode_group(pp, len(models), xyz_ptr, q, out_ptr, strict, stream))
+
+
+def inr_decode_grid(m, res, out_ptr, out_stride=None, ref_ptr=None, sse_ptr=None, stream=0):
+    r = (_I32 * 3)(*res)
+    s = (_I64 * 3)(*out_stride) if out_stride is not None else None
+    _check(_lib.inr_decode_grid(m, r, out_ptr, s, ref_ptr, sse_ptr, stream))
+
+
+def inr_value_range(view, minmax_ptr, stream=0):
+    _check(_lib.inr_value_range(ctypes.byref(view), minmax_ptr, stream))
+
+
+# ---- cache
+def cache_create(capacity, host_resident=0, device=0):
+    h = ctypes.c_void_p()
+    _check(_lib.cache_create(capacity, host_resident, device, ctypes.byref(h)))
+    return h
+
+
+def cache_destroy(c):
+    _check(_lib.cache_destroy(c))
+
+
+def cache_insert(c, timestep, models, stream=0):
+    pp, keep = _ptrs(models)
+    ev = _I64()
+    _check(_lib.cache_insert(c, timestep, pp, len(models), ctypes.byref(ev), stream))
+    return ev.value
+
+
+def cache_evict(c):
+    ev = _I64()
+    _check(_lib.cache_evict(c, ctypes.byref(ev)))
+    return ev.value
+
+
+def cache_size(c):
+    n = _I32()
+    _check(_lib.cache_size(c, ctypes.byref(n)))
+    return n.value
+
+
+def cache_bytes(c):
+    n = _I64()
+    _check(_lib.cache_bytes(c, ctypes.byref(n)))
+    return n.value
+
+
+def cache_get(c, i):
+    ts, nb = _I64(), _I32()
+    arr = _PP()
+    _check(_lib.cache_get(c, i, ctypes.byref(ts), ctypes.byref(arr), ctypes.byref(nb)))
+    return ts.value, [ctypes.c_void_p(arr[k]) for k in range(nb.value)]
+
+
+# ---- parity surface (host buffers are numpy float32 arrays)
+def _host(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def inr_get_params(m, out):
+    _check(_lib.inr_get_params(m, _host(out), out.size))
+    return out
+
+
+def inr_set_params(m, params):
+    _check(_lib.inr_set_params(m, _host(params), params.size))
+
+
+def inr_get_grads(m, out):
+    _check(_lib.inr_get_grads(m, _host(out), out.size))
+    return out
+
+
+def inr_get_adam_state(m, m_out, v_out):
+    _check(_lib.inr_get_adam_state(m, _host(m_out), _host(v_out), m_out.size))
+    return m_out, v_out
+
+
+def inr_debug_encode(m, x01_ptr, q, idx_ptr=None, feat_ptr=None, stream=0):
+    _check(_lib.inr_debug_encode(m, x01_ptr, q, idx_ptr, feat_ptr, stream))
+
+
+def inr_debug_forward(m, x01_ptr, q, y_ptr, stream=0):
+    _check(_lib.inr_debug_forward(m, x01_ptr, q, y_ptr, stream))
+
+
+def inr_kernel_launches():
+    return _lib.inr_kernel_launches()

@@ -1,0 +1,361 @@
+"""CUDA path vs oracle, element by element on the same seeded inputs
+(SURVEY.md §8(c) parity contract).  All calls go through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import adam as o_adam, decode as o_decode, encoding as o_enc, fit as o_fit, sampler
+from oracle.model import InrModel, init_params
+from paper_2304_10516_b200 import inr
+
+from gpu_util import (gpu_volume, get_grads, get_params, make_gpu_model, normwise, oracle_config, per_tensor_rel,
+                      stream, whole_view)
+
+pytestmark = pytest.mark.gpu
+
+CFG1 = dict(levels=8, features=2, log2_table_size=14, mlp_hidden_layers=2)
+CFG2 = dict(levels=16, features=2, log2_table_size=19, mlp_hidden_layers=3)
+
+
+@pytest.mark.parametrize("kw", [CFG1, CFG2, dict(levels=4, features=4, log2_table_size=12, mlp_hidden_layers=1),
+                                dict(levels=6, features=1, log2_table_size=10, mlp_hidden_layers=2, mlp_bias=0)])
+def test_init_bitwise(kw):
+    blk = sampler.decompose((64, 64, 64), (32, 32, 32))[5]
+    m = make_gpu_model(blk, 77, **kw)
+    try:
+        assert np.array_equal(get_params(m), init_params(oracle_config(**kw), 77, blk.block_id))
+    finally:
+        inr.inr_destroy(m)
+
+
+@pytest.mark.parametrize("kw", [CFG1, CFG2, dict(levels=8, features=8, log2_table_size=16, mlp_hidden_layers=1),
+                                dict(levels=12, features=1, log2_table_size=12, mlp_hidden_layers=1)])
+def test_encode_indices_bitexact_features_1e5(kw):
+    blk = sampler.decompose((64, 64, 64), (64, 64, 64))[0]
+    m = make_gpu_model(blk, 3, **kw)
+    cfg = oracle_config(**kw)
+    rng = np.random.default_rng(1)
+    p = rng.normal(size=cfg.param_count()).astype(np.float32)
+    inr.inr_set_params(m, p)
+    lat = np.stack(np.meshgrid(*[np.arange(9) / 8.0] * 3, indexing="ij"), -1).reshape(-1, 3)
+    x = np.concatenate([rng.random((5000, 3)), lat, [[1, 1, 1], [0, 0, 0], [1 - 2 ** -24] * 3]]).astype(np.float32)
+    q = x.shape[0]
+    xd = torch.from_numpy(x).cuda()
+    idx = torch.zeros(q * cfg.levels * 8, dtype=torch.int32, device="cuda")
+    feat = torch.zeros(q * cfg.levels * cfg.features, dtype=torch.float32, device="cuda")
+    inr.inr_debug_encode(m, xd.data_ptr(), q, idx.data_ptr(), feat.data_ptr(), stream())
+    torch.cuda.synchronize()
+    om = InrModel(cfg, blk, 3, params=p)
+    f_o, idx_o, _ = o_enc.encode_forward(om.tables(), x, cfg.resolutions(), cfg.table_size)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32).reshape(q, cfg.levels, 8), idx_o)
+    assert normwise(feat.cpu().numpy().reshape(q, -1), f_o) <= 1e-5
+    inr.inr_destroy(m)
+
+
+def test_forward_fp32_1e5():
+    blk = sampler.decompose((64, 64, 64), (64, 64, 64))[0]
+    for kw in (CFG1, CFG2):
+        cfg = oracle_config(**kw)
+        m = make_gpu_model(blk, 4, **kw)
+        rng = np.random.default_rng(2)
+        p = init_params(cfg, 4, 0)
+        p[: sum(cfg.level_sizes()) * cfg.features] = rng.uniform(-1, 1, sum(cfg.level_sizes()) * cfg.features)
+        inr.inr_set_params(m, p)
+        x = rng.random((3000, 3)).astype(np.float32)
+        xd = torch.from_numpy(x).cuda()
+        y = torch.zeros(3000, device="cuda")
+        inr.inr_debug_forward(m, xd.data_ptr(), 3000, y.data_ptr(), stream())
+        torch.cuda.synchronize()
+        yo, _ = o_fit.forward(InrModel(cfg, blk, 4, params=p), x)
+        assert normwise(y.cpu().numpy(), yo[:, 0]) <= 1e-5
+        inr.inr_destroy(m)
+
+
+def _perturbed_params(cfg, blk, seed, rng):
+    """Init parameters with O(0.1) tables and biases, so pre-activations sit
+    well away from the ReLU kink (at init the tables are ~1e-4)."""
+    p = init_params(cfg, seed, blk.block_id)
+    for name, shape, off in cfg.tensor_layout():
+        n = int(np.prod(shape))
+        if name.startswith("table") or name.startswith("b"):
+            p[off:off + n] = rng.uniform(-0.1, 0.1, n)
+    return p
+
+
+def _clean_seed(cfg, blk, vol, opts, batch, seeds, params, margin=1e-6):
+    """First seed whose step-0 batch keeps every |y - t| and every hidden
+    pre-activation at least `margin` away from the L1 / ReLU kinks, where GPU
+    fp32 and oracle fp64 could legitimately branch differently."""
+    for s in seeds:
+        om = InrModel(cfg, blk, s, params=params)
+        x_u, x_b, t_u, t_b, _ = o_fit.step_batch(om, vol, opts, batch)
+        x = np.concatenate([x_u, x_b])
+        y, cache = o_fit.forward(om, x)
+        t = np.concatenate([t_u, t_b])
+        zmin = min(float(np.min(np.abs(z))) for z in cache[3][:-1])
+        if float(np.min(np.abs(y[:, 0] - t))) > margin and zmin > margin:
+            return s, om
+    pytest.skip("no clean seed found")
+
+
+@pytest.mark.parametrize("det,prec,tol", [(1, 0, 1e-4), (0, 0, 1e-3), (1, 1, 3e-2)])
+def test_one_step_gradients_and_adam(det, prec, tol):
+    """Gradients of one fit step: per tensor ||d||_inf/||ref||_inf <= 1e-4 in the
+    deterministic fp32 mode (north_star), 1e-3 with fp32 atomics, 3e-2 with the
+    fp16 tensor-core MLP (fp16 operand rounding); then Adam."""
+    dims = (32, 32, 32)
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose(dims, (16, 16, 16))[3]          # has interior faces -> boundary term
+    lo, hi = sampler.value_range([vol])
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=128)
+    cfg = oracle_config(**CFG1)
+    p0 = _perturbed_params(cfg, blk, 1, np.random.default_rng(0))
+    seed, om = _clean_seed(cfg, blk, vol, opts, 512, range(100, 200), p0)
+    m = make_gpu_model(blk, seed, reduction=det, precision=prec, **CFG1)
+    inr.inr_set_params(m, p0)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, 128
+    rep = inr.inr_fit(m, whole_view(vt), 1, 512, go, stream())
+    l1u, l1b, _ = o_fit.train_step(om, vol, opts, 512)
+    g = get_grads(m)
+    err = per_tensor_rel(cfg, g, om.g)
+    print("per-tensor grad rel err", err)
+    assert err <= tol
+    lr = 1e-2
+    if prec == 0:
+        assert np.max(np.abs(get_params(m) - om.p)) <= 2e-4 * lr + 1e-7
+        assert abs(rep.loss_uniform - l1u) <= 1e-5 * l1u and abs(rep.loss_boundary - l1b) <= 1e-5 * l1b
+    else:
+        assert abs(rep.loss_uniform - l1u) <= 2e-3 * l1u and abs(rep.loss_boundary - l1b) <= 2e-3 * l1b
+    inr.inr_destroy(m)
+
+
+def test_forward_fp16_tensor_core_2e3():
+    """The tcgen05 fp16 MLP (fp32 accumulate) within 2e-3 normwise (north_star)."""
+    blk = sampler.decompose((64, 64, 64), (64, 64, 64))[0]
+    for kw in (CFG1, CFG2, dict(levels=16, features=4, log2_table_size=14, mlp_hidden_layers=4),
+               dict(levels=24, features=2, log2_table_size=12, mlp_hidden_layers=1, mlp_bias=0)):
+        cfg = oracle_config(**kw)
+        m = make_gpu_model(blk, 4, precision=1, **kw)
+        p = _perturbed_params(cfg, blk, 4, np.random.default_rng(3))
+        inr.inr_set_params(m, p)
+        x = np.random.default_rng(2).random((3001, 3)).astype(np.float32)
+        xd = torch.from_numpy(x).cuda()
+        y = torch.full((3001,), float("nan"), device="cuda")
+        inr.inr_debug_forward(m, xd.data_ptr(), 3001, y.data_ptr(), stream())
+        torch.cuda.synchronize()
+        yo, _ = o_fit.forward(InrModel(cfg, blk, 4, params=p), x)
+        err = normwise(y.cpu().numpy(), yo[:, 0])
+        print(kw, "fp16 forward normwise err", err)
+        assert err <= 2e-3
+        inr.inr_destroy(m)
+
+
+def test_deterministic_mode_bitwise_reproducible():
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[0]
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 256
+    out = []
+    for _ in range(2):
+        m = make_gpu_model(blk, 5, reduction=1, **CFG1)
+        inr.inr_fit(m, whole_view(vt), 5, 1024, go, stream())
+        out.append((get_params(m), get_grads(m)))
+        inr.inr_destroy(m)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_multi_step_adam_trajectory_close():
+    """Ten steps: parameters track the oracle (same samples each step)."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (32, 32, 32))[0]
+    lo, hi = sampler.value_range([vol])
+    cfg = oracle_config(**CFG1)
+    om = InrModel(cfg, blk, 8)
+    m = make_gpu_model(blk, 8, reduction=1, **CFG1)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = lo, hi
+    inr.inr_fit(m, whole_view(vt), 10, 256, go, stream())
+    o_fit.fit(om, vol, 10, 256, o_fit.FitOpts(vmin=lo, vmax=hi))
+    p = get_params(m)
+    d = np.abs(p - om.p)
+    assert np.median(d) < 1e-5 and inr.inr_steps(m) == 10
+    inr.inr_destroy(m)
+
+
+def test_decode_grid_and_query_vs_oracle():
+    vol = synth.g1_analytic(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    cfg = oracle_config(**CFG1)
+    rng = np.random.default_rng(12)
+    gms, oms = [], {}
+    for b in blocks:
+        p = init_params(cfg, 9, b.block_id)
+        p[: sum(cfg.level_sizes()) * 2] = rng.uniform(-1, 1, sum(cfg.level_sizes()) * 2)
+        m = make_gpu_model(b, 9, **CFG1)
+        inr.inr_set_params(m, p)
+        gms.append(m)
+        om = InrModel(cfg, b, 9, params=p)
+        oms[b.block_id] = om
+    # decode grid of block 5 at 1x and a ragged resolution
+    for res in ((16, 16, 16), (20, 7, 33)):
+        out = torch.empty(res[::-1], device="cuda")
+        inr.inr_decode_grid(gms[5], res, out.data_ptr(), None, None, None, stream())
+        torch.cuda.synchronize()
+        assert normwise(out.cpu().numpy(), o_decode.decode_grid(oms[5], res)) <= 1e-5
+    # strided write of every block into one global volume; == query at nodes, bitwise
+    full = torch.empty((32, 32, 32), device="cuda")
+    for m, b in zip(gms, blocks):
+        o = b.origin
+        base = full[o[2]:, o[1]:, o[0]:]
+        inr.inr_decode_grid(m, (16, 16, 16), base.data_ptr(), (1, 32, 1024), None, None, stream())
+    z, y, x = np.meshgrid(np.arange(32), np.arange(32), np.arange(32), indexing="ij")
+    pts = np.stack([x.ravel(), y.ravel(), z.ravel()], 1).astype(np.float32)
+    pd = torch.from_numpy(pts).cuda()
+    q = torch.empty(pts.shape[0], device="cuda")
+    inr.inr_decode_group(gms, pd.data_ptr(), pts.shape[0], q.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(q, full.reshape(-1))
+    # random queries vs the oracle router
+    rp = synth.random_points(4000, (32, 32, 32))
+    rd = torch.from_numpy(rp).cuda()
+    rq = torch.empty(4000, device="cuda")
+    inr.inr_decode_group(gms, rd.data_ptr(), 4000, rq.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    assert normwise(rq.cpu().numpy(), o_decode.decode_query(oms, rp)) <= 1e-5
+    # strict domain error
+    bad = torch.tensor([[-1.0, 0, 0]], device="cuda")
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_decode_group(gms, bad.data_ptr(), 1, rq.data_ptr(), 1, stream())
+    assert e.value.status == inr.INR_ERR_DOMAIN
+    for m in gms:
+        inr.inr_destroy(m)
+
+
+def test_decode_grid_sse_matches_oracle():
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (32, 32, 32))[0]
+    lo, hi = sampler.value_range([vol])
+    m = make_gpu_model(blk, 2, **CFG1)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = lo, hi
+    inr.inr_fit(m, whole_view(vt), 20, 1024, go, stream())
+    out = torch.empty((32, 32, 32), device="cuda")
+    sse = torch.zeros(1, dtype=torch.float64, device="cuda")
+    inr.inr_decode_grid(m, (32, 32, 32), out.data_ptr(), None, vt.data_ptr(), sse.data_ptr(), stream())
+    torch.cuda.synchronize()
+    want = o_decode.sse_normalized(out.cpu().numpy(), vol, lo, hi)
+    assert abs(sse.item() - want) <= 1e-6 * want
+    inr.inr_destroy(m)
+
+
+def test_value_range_exact():
+    vol = synth.g3_density(48).numpy()
+    vt = gpu_volume(vol)
+    mm = torch.tensor([float("inf"), float("-inf")], device="cuda")
+    inr.inr_value_range(whole_view(vt), mm.data_ptr(), stream())
+    sub = vt[8:40, 4:20, 0:48]
+    v2 = inr.make_view(sub.data_ptr(), (0, 4, 8), (48, 16, 32), (1, 48, 48 * 48))
+    mm2 = torch.tensor([float("inf"), float("-inf")], device="cuda")
+    inr.inr_value_range(v2, mm2.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert mm.tolist() == [float(vol.min()), float(vol.max())]
+    assert mm2.tolist() == [float(vol[8:40, 4:20].min()), float(vol[8:40, 4:20].max())]
+
+
+@pytest.mark.parametrize("host", [0, 1])
+def test_cache_fifo_and_decode_from_slot(host):
+    vol = synth.g1_analytic(16).numpy()
+    blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = float(vol.min()), float(vol.max())
+    m = make_gpu_model(blk, 1, **CFG1)
+    c = inr.cache_create(3, host, 0)
+    snaps = {}
+    for ts in (1, 2, 3, 4):
+        inr.inr_reset(m, 100 + ts)
+        inr.inr_fit(m, whole_view(vt), 3, 256, go, stream())
+        ev = inr.cache_insert(c, ts, [m], stream())
+        assert ev == (1 if ts == 4 else -1)
+        snaps[ts] = get_params(m)
+    assert inr.cache_size(c) == 3
+    assert inr.cache_bytes(c) == 3 * inr.inr_param_bytes(m)
+    with pytest.raises(inr.InrError):
+        inr.cache_insert(c, 4, [m], stream())
+    ts, blocks = inr.cache_get(c, 0)
+    assert ts == 2
+    assert np.array_equal(get_params(blocks[0]), snaps[2])
+    out = torch.empty((16, 16, 16), device="cuda")
+    inr.inr_decode_grid(blocks[0], (16, 16, 16), out.data_ptr(), None, None, None, stream())
+    inr.inr_set_params(m, snaps[2])
+    out2 = torch.empty((16, 16, 16), device="cuda")
+    inr.inr_decode_grid(m, (16, 16, 16), out2.data_ptr(), None, None, None, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_fit(blocks[0], whole_view(vt), 1, 16, go, stream())
+    assert e.value.status == inr.INR_ERR_STATE
+    assert inr.cache_evict(c) == 2 and inr.cache_evict(c) == 3 and inr.cache_evict(c) == 4
+    with pytest.raises(inr.InrError) as e:
+        inr.cache_evict(c)
+    assert e.value.status == inr.INR_ERR_STATE
+    inr.cache_destroy(c)
+    inr.inr_destroy(m)
+
+
+def test_group_fit_matches_single_fits():
+    """Blocks are independent: a grouped launch gives each model
+    the same result as fitting it alone (deterministic mode, bitwise)."""
+    vol = synth.g2_energy(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
+    group = [make_gpu_model(b, 6, reduction=1, **CFG1) for b in blocks]
+    reps = inr.inr_fit_group(group, [whole_view(vt)] * len(group), 6, 256, go, stream())
+    assert all(r.steps_taken == 6 for r in reps)
+    single = make_gpu_model(blocks[6], 6, reduction=1, **CFG1)
+    inr.inr_fit(single, whole_view(vt), 6, 256, go, stream())
+    assert np.array_equal(get_params(single), get_params(group[6]))
+    for m in group + [single]:
+        inr.inr_destroy(m)
+
+
+def test_fit_errors():
+    blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
+    m = make_gpu_model(blk, 1, **CFG1)
+    vt = gpu_volume(synth.g1_analytic(16).numpy())
+    go = inr.inr_fit_opts_default()
+    for steps, batch in ((0, 16), (1, 0)):
+        with pytest.raises(inr.InrError) as e:
+            inr.inr_fit(m, whole_view(vt), steps, batch, go, stream())
+        assert e.value.status == inr.INR_ERR_INVALID_ARG
+    go.lambda_ = 1.5
+    with pytest.raises(inr.InrError):
+        inr.inr_fit(m, whole_view(vt), 1, 16, go, stream())
+    go = inr.inr_fit_opts_default()
+    small = inr.make_view(vt.data_ptr(), (0, 0, 0), (8, 16, 16), (1, 16, 256))
+    with pytest.raises(inr.InrError):
+        inr.inr_fit(m, small, 1, 16, go, stream())
+    go.vmin = go.vmax = 0.5                                   # constant field: not an error
+    rep = inr.inr_fit(m, whole_view(vt), 2, 16, go, stream())
+    assert rep.constant_field == 1
+    inr.inr_destroy(m)
+
+
+def test_psnr_target_stopping():
+    vol = synth.constant_field((16, 16, 16), 0.5)
+    blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
+    m = make_gpu_model(blk, 5, **CFG1)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.lr0, go.target_psnr, go.check_interval = 0.0, 1.0, 1e-3, 45.0, 10
+    rep = inr.inr_fit(m, whole_view(vt), 400, 512, go, stream())
+    assert rep.reached_target == 1 and rep.probe_psnr >= 45 and rep.steps_taken < 400
+    inr.inr_destroy(m)
