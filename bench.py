@@ -1,0 +1,338 @@
+"""bench.py — fit coords/s (and decode voxels/s, PSNR @ ratio) of the hash-grid
+INR hot path on B200, per the BASELINE.json metric on configs[1]:
+
+  cfg2: a 256^3 CloverLeaf3D-shaped energy field (G2, tau =
+  0.35), 2x2x2 blocks of 128^3 on one GPU, L=16 T=2^19 F=2, 3x64 MLP,
+  B_u = 65536 uniform + B_b = 16384 boundary samples per block per step.
+
+A "step" is one fit iteration over all local blocks (sampling, targets,
+encode, MLP fwd, Eq. 2, MLP bwd, table scatter, Adam: §8(a) a2-a12).  Under
+torchrun each rank fits its own 8 blocks of a 256 x 256 x 256N volume (weak
+scaling; no collective inside the step).  `value` = coordinates fitted per
+second over all ranks (max-over-ranks device time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BLOCK = 128
+SIDE = 256
+CFG = dict(levels=16, features=2, log2_table_size=19, mlp_hidden_layers=3)
+B_U, B_B = 65536, 16384
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--precision", default="fp16", choices=["fp16", "fp32"])
+    p.add_argument("--psnr-steps", type=int, default=2000, help="total fit steps before the PSNR report (0: skip)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------- CPU legs
+def oracle_step_sample(steps, warmup, frac=0.25):
+    """The oracle (test infrastructure) as it stands, on a bounded sample: each
+    step is one fit step of ONE cfg2 block at `frac` of its batch.  Returns
+    (coords/s, cores, description)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    import synth
+    from oracle import fit as o_fit, sampler
+    from oracle.model import Config, InrModel
+    n = SIDE
+    vol = synth.g2_energy(n).numpy()
+    lo, hi = float(vol.min()), float(vol.max())
+    blk = sampler.decompose((n, n, n), (BLOCK,) * 3)[0]
+    bu, bb = int(B_U * frac), int(B_B * frac)
+    with threadpool_limits(1):
+        m = InrModel(Config(**CFG), blk, 1)
+        opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=bb)
+        for _ in range(warmup):
+            o_fit.train_step(m, vol, opts, bu)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o_fit.train_step(m, vol, opts, bu)
+        dt = time.perf_counter() - t0
+    coords = steps * (bu + bb)
+    desc = (f"{steps} oracle fit steps of one 128^3 cfg2 block at {bu}+{bb} coords/step "
+            f"(1/{int(8 / frac)} of a cfg2 step), numpy fp64, 1 thread")
+    return coords / dt, 1, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps, warm = max(1, args.steps), max(0, min(args.warmup, 1))
+    v, cores, desc = oracle_step_sample(steps, warm)
+    line = {
+        "metric": "fit_coords_per_s", "value": v, "unit": "coords/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
+        "dtype": "f64", "data": "synthetic", "config": workload_config(1, args),
+        "cpu_baseline": {"value": v, "unit": "coords/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": "coords/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world, args):
+    return {"workload": "cfg2: G2 256^3 CloverLeaf3D-shaped energy, 2x2x2 blocks of 128^3 per GPU, "
+                        "L16 T2^19 F2, 3x64 MLP, 65536+16384 coords/block/step",
+            "global_dims": [SIDE, SIDE, SIDE * world], "blocks_per_gpu": 8, "block": BLOCK,
+            "batch_uniform": B_U, "batch_boundary": B_B, "precision": args.precision,
+            "parallelism": f"blocks{world}" if world > 1 else "single",
+            "l2": "no flush: per-GPU working set (params+grads+Adam state 1.56 GB, volume 64 MB) >> 126 MB L2"}
+
+
+# ------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2304_10516_b200 import dnr, inr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream().cuda_stream
+    gdims = (SIDE, SIDE, SIDE * world)
+    prec = inr.INR_PREC_FP16_MLP if args.precision == "fp16" else inr.INR_PREC_FP32
+    cfg = inr.make_config(precision=prec, seed=0x230410516, **CFG)
+    d = dnr.DNR(gdims, (BLOCK,) * 3, cfg, rank, world, local)
+    lo, hi = d.lo, d.hi
+    # the rank's sub-volume (cores + 1-node high ghost layer), generated on the GPU
+    zs = torch.arange(lo[2], hi[2] + 1, dtype=torch.float64, device=dev)
+    vol = torch.empty((hi[2] - lo[2] + 1, hi[1] - lo[1] + 1, hi[0] - lo[0] + 1), dtype=torch.float32, device=dev)
+    for z0 in range(0, vol.shape[0], 16):
+        z1 = min(z0 + 16, vol.shape[0])
+        pos = synth.lattice(gdims, dev, (lo[2] + z0, lo[2] + z1))[:, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+        vol[z0:z1] = synth.evaluate("g2", pos, gdims).to(torch.float32)
+    del zs
+    vmin, vmax = d.value_range(vol, stream)                    # a1 + all-reduce MIN/MAX
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = B_B
+    nb = len(d.models)
+    coords_per_step = nb * (B_U + B_B)
+
+    # warm-up (untimed)
+    d.fit(vol, max(args.warmup, 1), B_U, opts, stream, report=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region: K fit steps, every kernel bracketed by CUDA events
+    launches0 = inr.inr_kernel_launches()
+    inr.inr_profile_enable(1)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    d.fit(vol, args.steps, B_U, opts, stream, report=False)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = inr.inr_kernel_launches() - launches0
+    prof = {k: inr.inr_profile_read(k) for k in ("step_begin", "fit_tc", "fit_fp32", "adam")}
+    inr.inr_profile_enable(0)
+    ms_max = dnr.allreduce_max(ms)
+    value = coords_per_step * world * args.steps / (ms_max / 1e3)
+
+    # ---- roofline of the dominant kernel (device time share)
+    P = inr.inr_param_count(d.models[0])
+    pk, pv = peaks()
+    kern = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(kern, key=lambda k: kern[k][0])
+    dom_ms, dom_n = kern[dom]
+    avg_s = dom_ms / dom_n / 1e3
+    if dom == "adam":
+        # algorithmic bytes: read p, g, m, v + write p, m, v (fp32) for every parameter of every block
+        alg = 28.0 * P * nb
+        roof = {"kernel": "adam", "bound": "hbm", "achieved": alg / avg_s / 1e9, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": alg}
+    else:
+        # the fused fit kernel: the dense contraction part on the tensor roofline
+        # (6 (LF W + (H-1) W^2 + W) FLOP per coordinate), plus its
+        # algorithmic L2 gather/scatter bytes (2 x 8 L F 4 B per coordinate)
+        LF, W, H = 32, 64, 3
+        flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])  # fp16 dense rate == bf16 on B200
+        roof = {"kernel": dom, "bound": "tensor", "achieved": flop / avg_s / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "traffic": None, "algorithmic_flop_per_launch": flop,
+                "l2_gather_scatter_bytes_per_launch": 2 * 8 * 16 * 2 * 4.0 * coords_per_step}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["peak_source"] = pv
+    roof["avg_launch_ms"] = avg_s * 1e3
+    roof["share_of_step"] = dom_ms / ms
+    kernels = {k: {"total_ms": v[0], "launches": v[1], "avg_ms": v[0] / max(v[1], 1)} for k, v in kern.items()}
+
+    # ---- end to end through the public API with host buffers: every step the
+    # volume is copied H2D from pinned memory, one fit step runs through
+    # inr_fit_group with a report (loss D2H)
+    host = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(vol)
+    vol2 = torch.empty_like(vol)
+    e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        vol2.copy_(host, non_blocking=True)
+        d.fit(vol2, 1, B_U, opts, stream, report=True)   # report => D2H of the losses + sync
+    torch.cuda.synchronize()
+    e_s = dnr.allreduce_max(time.perf_counter() - t0)
+    e2e = {"value": coords_per_step * world * e_steps / e_s, "unit": "coords/s",
+           "h2d_bytes_per_step": int(vol.numel() * 4), "d2h_bytes_per_step": int(nb * (8 * 2 + 4 + 8)),
+           "steps": e_steps, "clock": "host wall clock around synchronized steps, max over ranks"}
+
+    # ---- decode throughput (1x grid of the local cores) and PSNR @ ratio
+    out = torch.empty_like(vol)
+    sse = torch.zeros(1, dtype=torch.float64, device=dev)
+    d.decode_grid_local(out, 1, None, None, stream)                      # warm
+    torch.cuda.synchronize()
+    inr.inr_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    d.decode_grid_local(out, 1, None, None, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    dec_ms = dnr.allreduce_max(e0.elapsed_time(e1))
+    inr.inr_profile_enable(0)
+    vox_local = BLOCK ** 3 * len(d.models)
+    decode = {"voxels_per_s": vox_local * world / (dec_ms / 1e3), "ms": dec_ms, "voxels": vox_local * world,
+              "kernel": "decode_grid (fp32 CUDA-core MLP)"}
+    done = args.warmup + args.steps + e_steps
+    if args.psnr_steps > done:
+        d.fit(vol, args.psnr_steps - done, B_U, opts, stream, report=True)
+        done = args.psnr_steps
+    sse.zero_()
+    d.decode_grid_local(out, 1, vol, sse, stream)
+    torch.cuda.synchronize()
+    # core nodes only (the high ghost layer belongs to the next rank)
+    ncore = 1
+    for dd in range(3):
+        ncore *= (d.hi[dd] - d.lo[dd] + 1) if d.hi[dd] == gdims[dd] - 1 else (d.hi[dd] - d.lo[dd])
+    psnr = d.psnr(float(sse.item()), ncore)
+    raw_bytes = 4.0 * SIDE ** 3
+    ratio = raw_bytes / d.param_bytes()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, desc = oracle_step_sample(2, 0)
+        cpu = {"value": v, "unit": "coords/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "cpu": _cpu_model()}
+    if rank == 0:
+        line = {
+            "metric": "fit_coords_per_s", "value": value, "unit": "coords/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16-mlp/f32" if prec else "f32", "data": "synthetic",
+            "config": workload_config(world, args),
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "decode": decode, "psnr_db": psnr, "psnr_after_steps": done, "compression_ratio": ratio,
+            "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    d.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return None
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

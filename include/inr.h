@@ -126,13 +126,13 @@ INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
  *   target_psnr > 0 with check_interval > 0 stops once the PSNR on a 32^3
  *   cell-centred probe lattice reaches the target. */
 typedef struct {
-  float lambda;
+  double lambda;
   int32_t boundary_batch;
-  float lr0, lr_decay;
+  double lr0, lr_decay;
   int32_t lr_step;
-  float beta1, beta2, eps;
-  float vmin, vmax;
-  float target_psnr;
+  double beta1, beta2, eps;   /* double so that 1 - beta is exact as in PyTorch's Adam */
+  double vmin, vmax;
+  double target_psnr;
   int32_t check_interval;
 } inr_fit_opts;
 INR_API void inr_fit_opts_default(inr_fit_opts* o);
@@ -241,6 +241,14 @@ INR_API inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_
 /* Network output Phi(x) in normalized units for q block-normalized coordinates
  * (dev q x 3 -> dev q), in the model's configured precision.  Asynchronous. */
 INR_API inr_status inr_debug_forward(const inr_model* m, const float* x01, int64_t q, float* y, cudaStream_t stream);
+/* Kernel timing for benchmarks: while enabled, every kernel the library
+ * launches is bracketed by CUDA events recorded on its launching stream (and
+ * the fit loop does not use CUDA graphs).  inr_profile_read synchronizes and
+ * returns the summed device time (ms) and launch count of one kernel class:
+ * "step_begin", "fit_fp32", "fit_tc", "adam", "decode_grid", "decode_query",
+ * "probe", "range".  inr_profile_enable(1) also clears previous records. */
+INR_API inr_status inr_profile_enable(int32_t on);
+INR_API inr_status inr_profile_read(const char* kernel, double* total_ms, int64_t* launches);
 /* Number of kernels this library has launched since load (bench evidence). */
 INR_API int64_t inr_kernel_launches(void);
 

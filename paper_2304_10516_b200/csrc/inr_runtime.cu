@@ -57,6 +57,72 @@ static inr_status cuda_fail(cudaError_t e, const char* what) {
   } while (0)
 
 extern "C" const char* inr_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------ profiling
+enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_FIT_TC, PK_ADAM, PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE,
+                PK_COUNT };
+static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "fit_tc", "adam",
+                                           "decode_grid", "decode_query", "probe", "range"};
+struct ProfRec { int kind; cudaEvent_t a, b; };
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+static bool g_prof_on = false;
+
+static cudaEvent_t prof_event() {
+  cudaEvent_t e;
+  if (!g_event_pool.empty()) { e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one kernel launch with events on its stream when profiling is on.
+struct ProfScope {
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+    if (g_prof_on) { a = prof_event(); cudaEventRecord(a, st); }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, st);
+      g_prof.push_back({kind, a, b});
+    }
+  }
+};
+
+static void prof_clear() {
+  for (auto& r : g_prof) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
+  g_prof.clear();
+}
+
+extern "C" inr_status inr_profile_enable(int32_t on) {
+  g_prof_on = on != 0;
+  if (g_prof_on) prof_clear();
+  return INR_OK;
+}
+
+extern "C" inr_status inr_profile_read(const char* kernel, double* total_ms, int64_t* launches) {
+  if (!kernel || !total_ms || !launches) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  int kind = -1;
+  for (int k = 0; k < PK_COUNT; ++k)
+    if (!strcmp(kernel, kProfNames[k])) kind = k;
+  if (kind < 0) return fail(INR_ERR_INVALID_ARG, "unknown kernel class '%s'", kernel);
+  double ms = 0;
+  int64_t n = 0;
+  for (auto& r : g_prof) {
+    if (r.kind != kind) continue;
+    CK(cudaEventSynchronize(r.b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    ++n;
+  }
+  *total_ms = ms;
+  *launches = n;
+  return INR_OK;
+}
 extern "C" int64_t inr_kernel_launches(void) { return g_launches.load(); }
 
 // ------------------------------------------------------------------ model
@@ -283,17 +349,17 @@ extern "C" inr_status inr_steps(const inr_model* m, int64_t* steps) {
 
 extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
   if (!o) return;
-  o->lambda = 0.5f;
+  o->lambda = 0.5;
   o->boundary_batch = 0;
-  o->lr0 = 1e-2f;
-  o->lr_decay = 0.8f;
+  o->lr0 = 1e-2;
+  o->lr_decay = 0.8;
   o->lr_step = 500;
-  o->beta1 = 0.9f;
-  o->beta2 = 0.999f;
-  o->eps = 1e-8f;
-  o->vmin = 0.f;
-  o->vmax = 1.f;
-  o->target_psnr = 0.f;
+  o->beta1 = 0.9;
+  o->beta2 = 0.999;
+  o->eps = 1e-8;
+  o->vmin = 0.0;
+  o->vmax = 1.0;
+  o->target_psnr = 0.0;
   o->check_interval = 0;
 }
 
@@ -358,7 +424,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   if (!opts) return fail(INR_ERR_INVALID_ARG, "opts is NULL");
   if (steps < 1) return fail(INR_ERR_INVALID_ARG, "steps must be >= 1");
   if (batch < 1) return fail(INR_ERR_INVALID_ARG, "batch must be >= 1");
-  if (!(opts->lambda >= 0.f && opts->lambda <= 1.f)) return fail(INR_ERR_INVALID_ARG, "lambda must be in [0,1]");
+  if (!(opts->lambda >= 0.0 && opts->lambda <= 1.0)) return fail(INR_ERR_INVALID_ARG, "lambda must be in [0,1]");
   if (opts->boundary_batch < 0) return fail(INR_ERR_INVALID_ARG, "boundary_batch must be >= 0");
   if (opts->lr_step < 1) return fail(INR_ERR_INVALID_ARG, "lr_step must be >= 1");
   if (!(opts->vmax >= opts->vmin)) return fail(INR_ERR_INVALID_ARG, "vmax < vmin");
@@ -378,7 +444,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   FitScalars fs;
   fs.B_u = batch;
   fs.B_b = opts->boundary_batch;
-  fs.lambda = opts->lambda;
+  fs.lambda = (float)opts->lambda;
   fs.det = m0->cfg.reduction == INR_REDUCE_DETERMINISTIC;
   AdamScalars as;
   as.lr0 = opts->lr0;
@@ -386,11 +452,15 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   as.lr_step = opts->lr_step;
   as.beta1 = opts->beta1;
   as.beta2 = opts->beta2;
-  as.eps = opts->eps;
+  as.b1 = (float)opts->beta1;
+  as.b2 = (float)opts->beta2;
+  as.ob1 = (float)(1.0 - opts->beta1);
+  as.ob2 = (float)(1.0 - opts->beta2);
+  as.eps = (float)opts->eps;
 
   for (int i = 0; i < nmodels; ++i) {
-    models[i]->vmin = opts->vmin;
-    models[i]->vmax = opts->vmax;
+    models[i]->vmin = (float)opts->vmin;
+    models[i]->vmax = (float)opts->vmax;
   }
   const int nchunks = (nmodels + kMaxGroup - 1) / kMaxGroup;
   std::vector<GroupArgs> groups(nchunks);
@@ -413,18 +483,18 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   }
   auto enqueue_step = [&](cudaStream_t s) {
     for (int c = 0; c < nchunks; ++c) {
-      launch_step_begin(groups[c], groups[c].nmodels, s);
-      if (tc) launch_fit_tc(groups[c], groups[c].nmodels, fs, s);
-      else launch_fit_simt(groups[c], groups[c].nmodels, fs, s);
-      launch_adam(groups[c], groups[c].nmodels, as, s);
+      { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(groups[c], groups[c].nmodels, s); }
+      if (tc) { ProfScope p(PK_FIT_TC, s); launch_fit_tc(groups[c], groups[c].nmodels, fs, s); }
+      else { ProfScope p(PK_FIT_FP32, s); launch_fit_simt(groups[c], groups[c].nmodels, fs, s); }
+      { ProfScope p(PK_ADAM, s); launch_adam(groups[c], groups[c].nmodels, as, s); }
     }
   };
-  const bool probing = out && opts->target_psnr > 0.f && opts->check_interval > 0;
+  const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
   const int launches_per_step = 3 * nchunks;
   // Replay a captured step when there are enough steps to amortize capture and
   // the stream is capturable (not the legacy default stream).
   cudaGraphExec_t exec = nullptr;
-  if (steps >= 4 && st != nullptr) {
+  if (steps >= 4 && st != nullptr && !g_prof_on) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     long long before = g_launches.load();
@@ -454,7 +524,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       for (int c = 0; c < nchunks; ++c)
         for (int j = 0; j < groups[c].nmodels; ++j)
           CK(cudaMemsetAsync(groups[c].md[j].acc + 2, 0, sizeof(double), st));
-      for (int c = 0; c < nchunks; ++c) launch_probe(groups[c], groups[c].nmodels, st);
+      for (int c = 0; c < nchunks; ++c) { ProfScope p(PK_PROBE, st); launch_probe(groups[c], groups[c].nmodels, st); }
       CK_LAUNCH("probe");
       CK(cudaStreamSynchronize(st));
       reached_all = true;
@@ -523,7 +593,7 @@ extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], 
   else { os[0] = 1; os[1] = res[0]; os[2] = (long long)res[0] * res[1]; }
   int r[3] = {res[0], res[1], res[2]};
   ModelDev md = model_dev(m);
-  launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
+  { ProfScope p(PK_DECODE_GRID, st); launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st); }
   CK_LAUNCH("decode_grid");
   return INR_OK;
 }
@@ -571,7 +641,7 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
     if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int), st);
     if (e != cudaSuccess) { delete qa; return cuda_fail(e, "strict flag"); }
   }
-  if (q > 0) launch_decode_query_simt(*qa, xyz, q, out, dflag, st);
+  if (q > 0) { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_simt(*qa, xyz, q, out, dflag, st); }
   delete qa;
   CK_LAUNCH("decode_query");
   if (strict) {
@@ -601,7 +671,7 @@ extern "C" inr_status inr_value_range(const inr_view* v, float* minmax, cudaStre
     if (v->dims[d] < 1) return fail(INR_ERR_INVALID_ARG, "view dims must be >= 1");
   int dims[3] = {v->dims[0], v->dims[1], v->dims[2]};
   long long s[3] = {v->stride[0], v->stride[1], v->stride[2]};
-  launch_range(v->base, dims, s, minmax, st);
+  { ProfScope p(PK_RANGE, st); launch_range(v->base, dims, s, minmax, st); }
   CK_LAUNCH("value_range");
   return INR_OK;
 }

@@ -261,13 +261,13 @@ __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
   const ModelDev& md = g.md[blockIdx.y];
   const long long n = g.net.nparams;
   const long long s = *md.step_cur;
-  const double lr = (double)as.lr0 * pow((double)as.lr_decay, (double)(s / as.lr_step));
-  const double bc1 = 1.0 - pow((double)as.beta1, (double)(s + 1));
-  const double bc2 = 1.0 - pow((double)as.beta2, (double)(s + 1));
+  const double lr = as.lr0 * pow(as.lr_decay, (double)(s / as.lr_step));
+  const double bc1 = 1.0 - pow(as.beta1, (double)(s + 1));
+  const double bc2 = 1.0 - pow(as.beta2, (double)(s + 1));
   const float step_size = (float)(lr / bc1);
   const float inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
-  const float b1 = as.beta1, b2 = as.beta2, eps = as.eps;
-  const float ob1 = 1.f - b1, ob2 = 1.f - b2;
+  const float b1 = as.b1, b2 = as.b2, eps = as.eps;
+  const float ob1 = as.ob1, ob2 = as.ob2;
   const long long stride = (long long)gridDim.x * blockDim.x;
   bool bad = false;
   float* __restrict__ P = md.params;

@@ -22,9 +22,9 @@ struct FitScalars {
 };
 
 struct AdamScalars {
-  float lr0, lr_decay;
+  double lr0, lr_decay, beta1, beta2;
   long long lr_step;
-  float beta1, beta2, eps;
+  float b1, b2, ob1, ob2, eps;   // fp32 beta, 1 - beta (formed in fp64), eps
 };
 
 constexpr int kMaxRouteBlocks = 4096;

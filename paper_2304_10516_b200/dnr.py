@@ -1,0 +1,199 @@
+"""Distributed neural representation (DNR) shell: one process per GPU.
+
+PAPER.md L193-198: "creating a standard INR network on each MPI rank and
+training it using local data partitions ... without the need of data
+communication"; L205: all partitions use "the same maximum and minimum
+values".  Here a rank owns a contiguous z-major range of blocks
+(SURVEY.md §8(e)); torch.distributed (NCCL on GPUs, gloo on CPU for the host
+tests) is used only for the few reductions the method needs:
+
+  * before fitting: all-reduce MIN / MAX of the value range
+  * after fitting:  all-gather of per-block metadata
+  * after decoding: all-reduce SUM of the squared error -> PSNR
+  * optionally:     gather of decoded slabs to rank 0
+
+Nothing is communicated inside the fit loop.  All numerical work runs in
+libinr.so (paper_2304_10516_b200.inr); this module only marshals views and
+process-group calls.
+"""
+import math
+
+import torch
+import torch.distributed as dist
+
+# ------------------------------------------------------------------ host logic
+
+
+def block_grid(global_dims, n):
+    """Blocks per axis B_d = ceil(N_d / n_d) (x, y, z)."""
+    return tuple((int(N) + int(b) - 1) // int(b) for N, b in zip(global_dims, n))
+
+
+def block_origin(block_id, global_dims, n):
+    g = block_grid(global_dims, n)
+    bx = block_id % g[0]
+    by = (block_id // g[0]) % g[1]
+    bz = block_id // (g[0] * g[1])
+    return (bx * n[0], by * n[1], bz * n[2])
+
+
+def partition_blocks(nblocks, world, rank):
+    """Contiguous z-major range [r*NB/W, (r+1)*NB/W) of block ids."""
+    lo = (rank * nblocks) // world
+    hi = ((rank + 1) * nblocks) // world
+    return list(range(lo, hi))
+
+
+def local_node_box(block_ids, global_dims, n):
+    """Node box (lo, hi inclusive) covering the given blocks' cores plus the
+    1-node high-side ghost layer each block's view needs (R6)."""
+    lo = [None] * 3
+    hi = [None] * 3
+    for b in block_ids:
+        o = block_origin(b, global_dims, n)
+        for d in range(3):
+            a = o[d]
+            e = min(o[d] + n[d], global_dims[d] - 1)
+            lo[d] = a if lo[d] is None else min(lo[d], a)
+            hi[d] = e if hi[d] is None else max(hi[d], e)
+    return tuple(lo), tuple(hi)
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def allreduce_range(vmin, vmax):
+    """Global (vmin, vmax) over ranks: all-reduce MIN and MAX."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(vmin), float(vmax)
+    t = torch.tensor([float(vmin), -float(vmax)], dtype=torch.float64, device=_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t[0]), float(-t[1])
+
+
+def allreduce_sum(values):
+    """Element-wise SUM over ranks of a list of floats (fp64), e.g. (SSE, count)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def allreduce_max(value):
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def allgather_metadata(rows):
+    """All-gather per-block metadata rows (lists of floats) from every rank,
+    returned in rank order ("synchronizes the metadata")."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(rows)
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, list(rows))
+    return [r for part in out for r in part]
+
+
+def psnr_from_sse(sse, count):
+    """PSNR = -10 log10(MSE), capped at 200 dB (R18)."""
+    if count <= 0:
+        return 0.0
+    mse = sse / count
+    return 200.0 if mse <= 0 else min(200.0, -10.0 * math.log10(mse))
+
+
+# ------------------------------------------------------------------ device side
+
+
+class DNR:
+    """The blocks of one rank, their libinr models and their views into the
+    rank's local sub-volume (a CUDA tensor [z, y, x] covering local_node_box)."""
+
+    def __init__(self, global_dims, n, cfg, rank=0, world=1, device=None):
+        from . import inr  # the CUDA library; fails loudly if it is not built
+        self.inr = inr
+        self.global_dims = tuple(int(v) for v in global_dims)
+        self.n = tuple(int(v) for v in n)
+        g = block_grid(self.global_dims, self.n)
+        self.nblocks = g[0] * g[1] * g[2]
+        self.block_ids = partition_blocks(self.nblocks, world, rank)
+        self.rank, self.world = rank, world
+        self.device = torch.cuda.current_device() if device is None else device
+        self.lo, self.hi = local_node_box(self.block_ids, self.global_dims, self.n)
+        self.cfg = cfg
+        self.models = []
+        for b in self.block_ids:
+            o = block_origin(b, self.global_dims, self.n)
+            self.models.append(inr.inr_create(cfg, inr.make_block(o, self.n, self.global_dims), self.device))
+        self.vmin, self.vmax = 0.0, 1.0
+
+    def local_dims(self):
+        """(nx, ny, nz) of the local sub-volume."""
+        return tuple(h - l + 1 for l, h in zip(self.lo, self.hi))
+
+    def views(self, local_volume):
+        """One view per local block into the local sub-volume (zero-copy)."""
+        nz, ny, nx = local_volume.shape
+        assert (nx, ny, nz) == self.local_dims(), (local_volume.shape, self.local_dims())
+        v = self.inr.make_view(local_volume.data_ptr(), self.lo, (nx, ny, nz), (1, nx, nx * ny))
+        return [v] * len(self.models)
+
+    def value_range(self, local_volume, stream=0):
+        """Min/max over this rank's core nodes (libinr range kernel), then the
+        all-reduce (a1)."""
+        nz, ny, nx = local_volume.shape
+        mm = torch.tensor([float("inf"), float("-inf")], device=local_volume.device)
+        # core nodes only: the high ghost layer belongs to the next rank's blocks
+        core_hi = [min(h, self.hi[d] if self.hi[d] == self.global_dims[d] - 1 else self.hi[d] - 1)
+                   for d, h in enumerate(self.hi)]
+        dims = tuple(core_hi[d] - self.lo[d] + 1 for d in range(3))
+        v = self.inr.make_view(local_volume.data_ptr(), self.lo, dims, (1, nx, nx * ny))
+        self.inr.inr_value_range(v, mm.data_ptr(), stream)
+        torch.cuda.current_stream().synchronize()
+        lo, hi = mm.tolist()
+        self.vmin, self.vmax = allreduce_range(lo, hi)
+        return self.vmin, self.vmax
+
+    def fit(self, local_volume, steps, batch, opts, stream=0, report=True):
+        """inr_fit_group over the local blocks (no communication), then the
+        metadata all-gather when a report is requested."""
+        opts.vmin, opts.vmax = self.vmin, self.vmax
+        reps = self.inr.inr_fit_group(self.models, self.views(local_volume), steps, batch, opts, stream, report)
+        if not report:
+            return None
+        rows = [[float(b), float(r.steps_taken), r.loss_uniform, r.loss_boundary, r.probe_psnr]
+                for b, r in zip(self.block_ids, reps)]
+        return allgather_metadata(rows)
+
+    def decode_grid_local(self, out, scale=1, ref=None, sse=None, stream=0):
+        """Decode every local block at `scale` x resolution into `out`, a tensor
+        [z, y, x] covering the local cores at that resolution (strided writes,
+        no copies); optional fused SSE against `ref` (same layout)."""
+        nz, ny, nx = out.shape
+        res = tuple(int(b * scale) for b in self.n)
+        for b, m in zip(self.block_ids, self.models):
+            o = block_origin(b, self.global_dims, self.n)
+            off = [(o[d] - self.lo[d]) * scale for d in range(3)]
+            # a block at the upper domain face decodes the lattice points up to N (R19)
+            r = tuple(min(res[d], (self.global_dims[d] - o[d]) * scale) for d in range(3))
+            base = out[off[2]:, off[1]:, off[0]:]
+            refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
+            self.inr.inr_decode_grid(m, r, base.data_ptr(), (1, nx, nx * ny), refp,
+                                     sse.data_ptr() if sse is not None else None, stream)
+
+    def psnr(self, sse_local, count_local):
+        sse, cnt = allreduce_sum([sse_local, count_local])
+        return psnr_from_sse(sse, cnt)
+
+    def param_bytes(self):
+        return sum(self.inr.inr_param_bytes(m) for m in self.models)
+
+    def close(self):
+        for m in self.models:
+            self.inr.inr_destroy(m)
+        self.models = []

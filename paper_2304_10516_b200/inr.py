@@ -47,10 +47,10 @@ class inr_block(ctypes.Structure):
 
 
 class inr_fit_opts(ctypes.Structure):
-    _fields_ = [("lambda_", ctypes.c_float), ("boundary_batch", ctypes.c_int32), ("lr0", ctypes.c_float),
-                ("lr_decay", ctypes.c_float), ("lr_step", ctypes.c_int32), ("beta1", ctypes.c_float),
-                ("beta2", ctypes.c_float), ("eps", ctypes.c_float), ("vmin", ctypes.c_float),
-                ("vmax", ctypes.c_float), ("target_psnr", ctypes.c_float), ("check_interval", ctypes.c_int32)]
+    _fields_ = [("lambda_", ctypes.c_double), ("boundary_batch", ctypes.c_int32), ("lr0", ctypes.c_double),
+                ("lr_decay", ctypes.c_double), ("lr_step", ctypes.c_int32), ("beta1", ctypes.c_double),
+                ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("vmin", ctypes.c_double),
+                ("vmax", ctypes.c_double), ("target_psnr", ctypes.c_double), ("check_interval", ctypes.c_int32)]
 
 
 class inr_fit_report(ctypes.Structure):
@@ -98,6 +98,8 @@ _SIG = {
     "inr_debug_encode": (_I32, [_P, _P, _I64, _P, _P, _P]),
     "inr_debug_forward": (_I32, [_P, _P, _I64, _P, _P]),
     "inr_kernel_launches": (_I64, []),
+    "inr_profile_enable": (_I32, [_I32]),
+    "inr_profile_read": (_I32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(_lib, _name)
@@ -286,3 +288,14 @@ def inr_debug_forward(m, x01_ptr, q, y_ptr, stream=0):
 
 def inr_kernel_launches():
     return _lib.inr_kernel_launches()
+
+
+def inr_profile_enable(on=1):
+    _check(_lib.inr_profile_enable(on))
+
+
+def inr_profile_read(kernel):
+    """(total device ms, launches) of one kernel class since inr_profile_enable(1)."""
+    ms, n = ctypes.c_double(), _I64()
+    _check(_lib.inr_profile_read(kernel.encode(), ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

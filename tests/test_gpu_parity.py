@@ -99,11 +99,21 @@ def _clean_seed(cfg, blk, vol, opts, batch, seeds, params, margin=1e-6):
     pytest.skip("no clean seed found")
 
 
-@pytest.mark.parametrize("det,prec,tol", [(1, 0, 1e-4), (0, 0, 1e-3), (1, 1, 3e-2)])
-def test_one_step_gradients_and_adam(det, prec, tol):
-    """Gradients of one fit step: per tensor ||d||_inf/||ref||_inf <= 1e-4 in the
-    deterministic fp32 mode (north_star), 1e-3 with fp32 atomics, 3e-2 with the
-    fp16 tensor-core MLP (fp16 operand rounding); then Adam."""
+def _adam_reference(p0, g, lr=1e-2):
+    """The oracle's Adam (PyTorch form, pinned in test_oracle_pins) applied to the
+    GPU's own gradients: isolates the Adam kernel from gradient rounding, which
+    Adam amplifies by lr/eps = 1e6 for |g| ~ eps."""
+    p = p0.astype(np.float64).copy()
+    m, v = np.zeros_like(p), np.zeros_like(p)
+    o_adam.adam_update(p, g.astype(np.float64), m, v, 1, lr)
+    return p, m, v
+
+
+@pytest.mark.parametrize("det,tol", [(1, 1e-4), (0, 1e-3)])
+def test_one_step_gradients_and_adam_fp32(det, tol):
+    """Gradients of one fit step in the fp32 mode: per tensor
+    ||d||_inf/||ref||_inf <= 1e-4 with the deterministic reduction (north_star),
+    1e-3 with fp32 atomics; the Adam update of those gradients to 1e-6."""
     dims = (32, 32, 32)
     vol = synth.g1_analytic(32).numpy()
     blk = sampler.decompose(dims, (16, 16, 16))[3]          # has interior faces -> boundary term
@@ -112,7 +122,7 @@ def test_one_step_gradients_and_adam(det, prec, tol):
     cfg = oracle_config(**CFG1)
     p0 = _perturbed_params(cfg, blk, 1, np.random.default_rng(0))
     seed, om = _clean_seed(cfg, blk, vol, opts, 512, range(100, 200), p0)
-    m = make_gpu_model(blk, seed, reduction=det, precision=prec, **CFG1)
+    m = make_gpu_model(blk, seed, reduction=det, **CFG1)
     inr.inr_set_params(m, p0)
     vt = gpu_volume(vol)
     go = inr.inr_fit_opts_default()
@@ -123,12 +133,52 @@ def test_one_step_gradients_and_adam(det, prec, tol):
     err = per_tensor_rel(cfg, g, om.g)
     print("per-tensor grad rel err", err)
     assert err <= tol
-    lr = 1e-2
-    if prec == 0:
-        assert np.max(np.abs(get_params(m) - om.p)) <= 2e-4 * lr + 1e-7
-        assert abs(rep.loss_uniform - l1u) <= 1e-5 * l1u and abs(rep.loss_boundary - l1b) <= 1e-5 * l1b
-    else:
-        assert abs(rep.loss_uniform - l1u) <= 2e-3 * l1u and abs(rep.loss_boundary - l1b) <= 2e-3 * l1b
+    assert abs(rep.loss_uniform - l1u) <= 1e-5 * l1u and abs(rep.loss_boundary - l1b) <= 1e-5 * l1b
+    pe, me, ve = _adam_reference(p0, g)
+    mg, vg = inr.inr_get_adam_state(m, np.empty_like(g), np.empty_like(g))
+    assert np.max(np.abs(get_params(m) - pe)) <= 1e-6 * 1e-2 + 1e-7 * np.abs(pe).max()
+    assert np.allclose(mg, me, rtol=1e-6, atol=0) and np.allclose(vg, ve, rtol=1e-5, atol=1e-30)
+    inr.inr_destroy(m)
+
+
+def _linear_regime_params(cfg, blk, rng):
+    """O(0.1) tables and large positive biases: every ReLU is active (the MLP is
+    linear on the batch), so GPU and oracle cannot branch differently."""
+    p = _perturbed_params(cfg, blk, 1, rng)
+    for name, shape, off in cfg.tensor_layout():
+        if name.startswith("b"):
+            k = int(name[1:])
+            p[off:off + int(np.prod(shape))] = 0.0 if k == cfg.mlp_hidden_layers else 1.0 + 7.0 * k
+    return p
+
+
+@pytest.mark.parametrize("prec,tol", [(0, 1e-5), (1, 1e-2)])
+def test_one_step_gradients_linear_regime(prec, tol):
+    """Flip-free gradient parity (targets far below the outputs: sgn(y-t) = +1
+    everywhere; all ReLUs active).  Isolates the backward arithmetic of the fp16
+    tensor-core MLP (fp16 operands, fp32 TMEM accumulation, 2^k loss scaling),
+    whose realistic-batch comparison is dominated by legitimate L1/ReLU branch
+    flips of samples within fp16 rounding of a kink (R27)."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[3]
+    lo, hi = float(vol.max()) + 50.0, float(vol.max()) + 51.0    # t ~ -50 << y
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=128)
+    cfg = oracle_config(**CFG1)
+    p0 = _linear_regime_params(cfg, blk, np.random.default_rng(5))
+    om = InrModel(cfg, blk, 7, params=p0)
+    x_u, x_b, _, _, _ = o_fit.step_batch(om, vol, opts, 1000)
+    _, cache = o_fit.forward(om, np.concatenate([x_u, x_b]))
+    assert min(float(z.min()) for z in cache[3][:-1]) > 0.05
+    m = make_gpu_model(blk, 7, reduction=1, precision=prec, **CFG1)
+    inr.inr_set_params(m, p0)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, 128
+    inr.inr_fit(m, whole_view(vt), 1, 1000, go, stream())
+    o_fit.train_step(om, vol, opts, 1000)
+    err = per_tensor_rel(cfg, get_grads(m), om.g)
+    print("precision", prec, "per-tensor grad rel err", err)
+    assert err <= tol
     inr.inr_destroy(m)
 
 
