@@ -1,0 +1,72 @@
+"""Host-side logic of the multi-GPU shell (dnr.py) on CPU: block
+partitioning, and the only collectives the method needs (P:L193-205:
+range MIN/MAX before fitting, SSE SUM and metadata all-gather after), run
+with world_size 2 over gloo."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2304_10516_b200 import dnr
+
+
+def test_partition_is_contiguous_and_covers():
+    for nb, w in ((8, 1), (64, 8), (64, 3), (7, 4), (512, 8)):
+        parts = [dnr.partition_blocks(nb, w, r) for r in range(w)]
+        flat = [b for p in parts for b in p]
+        assert flat == list(range(nb))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def test_block_geometry_and_local_box():
+    g = (256, 256, 512)
+    assert dnr.block_grid(g, (128, 128, 128)) == (2, 2, 4)
+    assert dnr.block_origin(5, g, (128,) * 3) == (128, 0, 128)
+    ids = dnr.partition_blocks(16, 2, 0)                    # z rows 0..1
+    assert dnr.local_node_box(ids, g, (128,) * 3) == ((0, 0, 0), (255, 255, 256))
+    ids = dnr.partition_blocks(16, 2, 1)
+    assert dnr.local_node_box(ids, g, (128,) * 3) == ((0, 0, 256), (255, 255, 511))
+
+
+def test_psnr_from_sse():
+    assert dnr.psnr_from_sse(0.0, 10) == 200.0
+    assert abs(dnr.psnr_from_sse(0.01 * 10, 10) - 20.0) < 1e-12
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = [(0.0, 1.0), (-2.0, 0.5)][rank]
+    rng = dnr.allreduce_range(lo, hi)
+    sse = dnr.allreduce_sum([0.5 * (rank + 1), 100.0])
+    meta = dnr.allgather_metadata([[float(rank), 10.0 + rank]])
+    mx = dnr.allreduce_max(3.0 * rank)
+    q.put((rank, rng, sse, meta, mx))
+    dist.destroy_process_group()
+
+
+def test_collectives_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(60)
+    for rank, rng, sse, meta, mx in res:
+        assert rng == (-2.0, 1.0)                         # S:L275-277 example
+        assert sse == [1.5, 200.0]
+        assert meta == [[0.0, 10.0], [1.0, 11.0]]
+        assert mx == 3.0
