@@ -59,10 +59,10 @@ static inr_status cuda_fail(cudaError_t e, const char* what) {
 extern "C" const char* inr_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ profiling
-enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_FIT_TC, PK_ADAM, PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE,
-                PK_COUNT };
-static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "fit_tc", "adam",
-                                           "decode_grid", "decode_query", "probe", "range"};
+enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_SAMPLE, PK_ENCODE_FWD, PK_MLP_TC, PK_ENCODE_BWD, PK_ADAM,
+                PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE, PK_COUNT };
+static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "sample", "encode_fwd", "mlp_tc", "encode_bwd",
+                                           "adam", "decode_grid", "decode_query", "probe", "range"};
 struct ProfRec { int kind; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_event_pool;
@@ -481,16 +481,37 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       for (int k = 0; k < 3; ++k) { d.vlo[k] = v.lo[k]; d.vstride[k] = v.stride[k]; }
     }
   }
+  // fp16 path: level-major pipeline with a per-call workspace (stream-ordered allocation)
+  void* ws_mem = nullptr;
+  LmWorkspace ws{};
+  if (tc) {
+    const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
+    const int per = std::min(nmodels, kMaxGroup);
+    CK(cudaMallocAsync(&ws_mem, lm_workspace_bytes(m0->net, per, Bs), st));
+    ws = lm_workspace(ws_mem, m0->net, per, Bs);
+  }
   auto enqueue_step = [&](cudaStream_t s) {
     for (int c = 0; c < nchunks; ++c) {
-      { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(groups[c], groups[c].nmodels, s); }
-      if (tc) { ProfScope p(PK_FIT_TC, s); launch_fit_tc(groups[c], groups[c].nmodels, fs, s); }
-      else { ProfScope p(PK_FIT_FP32, s); launch_fit_simt(groups[c], groups[c].nmodels, fs, s); }
-      { ProfScope p(PK_ADAM, s); launch_adam(groups[c], groups[c].nmodels, as, s); }
+      const GroupArgs& g = groups[c];
+      { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, s); }
+      if (tc) {
+        { ProfScope p(PK_SAMPLE, s); launch_sample(g, g.nmodels, fs, ws, s); }
+        { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
+        { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.feat, ws.samples, ws.dfeat, ws.Bs, s); }
+        { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, ws, s); }
+      } else {
+        ProfScope p(PK_FIT_FP32, s);
+        launch_fit_simt(g, g.nmodels, fs, s);
+      }
+      { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
     }
   };
+  struct WsFree {
+    void*& p; cudaStream_t s;
+    ~WsFree() { if (p) cudaFreeAsync(p, s); }
+  } ws_free{ws_mem, st};
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = 3 * nchunks;
+  const int launches_per_step = (tc ? 6 : 3) * nchunks;
   // Replay a captured step when there are enough steps to amortize capture and
   // the stream is capturable (not the legacy default stream).
   cudaGraphExec_t exec = nullptr;

@@ -24,231 +24,130 @@
 // that need it without a transposed copy.
 #include <algorithm>
 
-#include "common.cuh"
 #include "launch.h"
+#include "tc_common.cuh"
 
 namespace inr {
 
-namespace tc {
 
-constexpr int kThreads = 128;
-constexpr int kTileM = 128;
-
-struct Layout {
-  uint32_t w[kMaxLayers];        // fp16 W_k tile [64 x in_k] (k < H)
-  uint32_t w_sbo[kMaxLayers];
-  uint32_t h[kMaxLayers];        // fp16 h_k tile [128 x (in_k + ones)] (k < H), h_0 = features
-  uint32_t h_sbo[kMaxLayers];
-  uint32_t dz, dz_sbo;           // fp16 dz tile [128 x 64]
-  uint32_t bias;                 // fp32 [H][64]
-  uint32_t wout;                 // fp32 W_H[64], then b_H
-  uint32_t red;                  // fp32 dW_H[64], db_H, pad
-  uint32_t mbar;                 // 8 B
-  uint32_t tslot;                // 4 B: TMEM base address
-  uint32_t bytes;                // dynamic smem requested
-  uint32_t col_dw[kMaxLayers];   // TMEM column of the dW_k accumulator
-  uint32_t ncols;                // TMEM columns allocated (power of 2)
-  int ones;                      // 8 if biases (ones group appended), else 0
-  int ctas_per_sm;
-};
-
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
-  return d;
-}
-
-// kind::f16 instruction descriptor: fp16 A/B, fp32 D.
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(mbar)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(mbar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-
-// 16 consecutive fp32 columns of this thread's TMEM lane.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// Row r of a canonical tile: write 8 consecutive columns [8j, 8j+8) as fp16.
-__device__ __forceinline__ void st_row8(uint8_t* tile, uint32_t sbo, int r, int j, const float* v) {
-  __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
-  __half2 h2 = __floats2half2_rn(v[4], v[5]), h3 = __floats2half2_rn(v[6], v[7]);
-  uint4 u;
-  u.x = *reinterpret_cast<uint32_t*>(&h0);
-  u.y = *reinterpret_cast<uint32_t*>(&h1);
-  u.z = *reinterpret_cast<uint32_t*>(&h2);
-  u.w = *reinterpret_cast<uint32_t*>(&h3);
-  *reinterpret_cast<uint4*>(tile + (r & 7) * 16 + (r >> 3) * sbo + j * 128) = u;
-}
-
-__device__ __forceinline__ uint32_t tile_off(uint32_t sbo, int r, int c) {
-  return (r & 7) * 16 + (r >> 3) * sbo + (c >> 3) * 128 + (c & 7) * 2;
-}
-
-// Sum 64 per-lane values over the warp; lane l ends with the column sums of
-// columns c0 = 32 b4 + 16 b3 + 8 b2 + 4 b1 + 2 b0 and c0 + 1 (b = lane bits).
-__device__ __forceinline__ void warp_transpose_reduce64(float* v, int lane) {
-#pragma unroll
-  for (int half = 32, off = 16; off >= 1; half >>= 1, off >>= 1) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int j = 0; j < half; ++j) {
-      float keep = up ? v[j + half] : v[j];
-      float send = up ? v[j] : v[j + half];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-}
-
-}  // namespace tc
 
 using namespace tc;
 
-// Issue the K loop of one GEMM (single thread).  a/b: start addresses; the
-// per-K-step (16 elements) advance of each operand is given explicitly.
-__device__ __forceinline__ void gemm(uint32_t tmem_d, uint32_t a, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_step,
-                                     uint32_t b, uint32_t b_lbo, uint32_t b_sbo, uint32_t b_step, int ksteps,
-                                     uint32_t idesc, bool accum_first) {
-  for (int k = 0; k < ksteps; ++k) {
-    uint64_t ad = make_desc(a + k * a_step, a_lbo, a_sbo);
-    uint64_t bd = make_desc(b + k * b_step, b_lbo, b_sbo);
-    mma_f16(tmem_d, ad, bd, idesc, (k > 0 || accum_first) ? 1u : 0u);
-  }
-}
-
-template <int F>
-__global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitScalars fs, Layout lay,
-                                                            float loss_scale) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const NetDesc& net = g.net;
-  const ModelDev& md = g.md[blockIdx.y];
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int H = net.H, LF = net.LF, ones = lay.ones;
-  const int B_b = md.nfaces > 0 ? fs.B_b : 0;
-  const int total = fs.B_u + B_b;
-  const int ntiles = (total + kTileM - 1) / kTileM;
-  const float* __restrict__ P = md.params;
-  float* __restrict__ G = md.grads;
-  unsigned long long* __restrict__ GX = md.grads_fx;
-  const float inv_scale = 1.f / loss_scale;
-
+// Load this CTA's copy of the network (fp16 weight tiles, fp32 biases and output
+// layer), allocate TMEM and initialise the MMA-completion mbarrier.
+__device__ __forceinline__ uint32_t mlp_setup(const NetDesc& net, const float* __restrict__ P, uint8_t* smem,
+                                              const Layout& lay, bool ones_groups) {
+  const int t = threadIdx.x, warp = t >> 5;
+  const int H = net.H;
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
-  float* red = reinterpret_cast<float*>(smem + lay.red);
-  const uint32_t mbar = smem_u32(smem + lay.mbar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
-
-  // ---- setup: TMEM allocation, barrier, weights -> fp16 tiles, constants
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
                  "r"(lay.ncols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (t == 0) {
-    mbar_init(mbar, 1);
+    mbar_init(smem_u32(smem + lay.mbar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int k = 0; k < H; ++k) {
     const int in = net.in_dim[k];
     const float* W = P + net.w_off[k];
-    for (int e = t; e < 64 * in; e += kThreads) {
+    for (int e = t; e < 64 * in; e += blockDim.x) {
       int n = e / in, i = e - n * in;
       *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) = __float2half_rn(W[e]);
     }
-    for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
-    if (ones) {  // constant ones group of h_k: column in_k = 1, in_k+1..+7 = 0
-      uint4 u = make_uint4(0x3C00u, 0u, 0u, 0u);  // half(1.0) in the low half of the first word
+    for (int n = t; n < 64; n += blockDim.x) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
+    if (ones_groups && lay.ones && t < kTileM) {  // constant ones group of h_k: column in_k = 1, in_k+1..+7 = 0
+      uint4 u = make_uint4(0x3C00u, 0u, 0u, 0u);   // half(1.0) in the low half of the first word
       *reinterpret_cast<uint4*>(smem + lay.h[k] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[k] + (in >> 3) * 128) = u;
     }
   }
-  for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
+  for (int i = t; i < 64; i += blockDim.x) wout[i] = P[net.w_off[H] + i];
   if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
-  for (int i = t; i < 66; i += kThreads) red[i] = 0.f;
   fence_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tmem = *tslot;
+  return *tslot;
+}
+
+__device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(lay.ncols));
+}
+
+// ---------------------------------------------------------------------------
+// MLP forward + Eq. 2 + backward on tensor cores for level-major features
+// (the middle kernel of the fp16 fit pipeline).  feat: fp16 [model][level][Bs][F],
+// samples: float4 (x, y, z, target) [model][Bs]; writes dfeat fp32
+// [model][level][Bs][F]; adds dW, db into the model's gradient.
+template <int F>
+__global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitScalars fs, Layout lay,
+                                                             float loss_scale, const __half* __restrict__ feat,
+                                                             const float4* __restrict__ samples,
+                                                             float* __restrict__ dfeat, int Bs) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const NetDesc& net = g.net;
+  const int m = blockIdx.y;
+  const ModelDev& md = g.md[m];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int H = net.H, L = net.L, ones = lay.ones;
+  const int B_b = md.nfaces > 0 ? fs.B_b : 0;
+  const int total = fs.B_u + B_b;
+  const int ntiles = (total + kTileM - 1) / kTileM;
+  float* __restrict__ G = md.grads;
+  unsigned long long* __restrict__ GX = md.grads_fx;
+  const float inv_scale = 1.f / loss_scale;
+  const __half* featm = feat + (size_t)m * L * Bs * F;
+  float* dfeatm = dfeat + (size_t)m * L * Bs * F;
+
+  float* bias = reinterpret_cast<float*>(smem + lay.bias);
+  float* wout = reinterpret_cast<float*>(smem + lay.wout);
+  float* red = reinterpret_cast<float*>(smem + lay.red);
+  const uint32_t mbar = smem_u32(smem + lay.mbar);
+  for (int i = t; i < 66; i += kThreads) red[i] = 0.f;
+  const uint32_t tmem = mlp_setup(net, md.params, smem, lay, true);
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0;
   bool first = true;
-  const uint32_t step = (uint32_t)*md.step_cur;
   const float lam = B_b > 0 ? fs.lambda : 0.f;
 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int i = tile * kTileM + t;
     const bool valid = i < total;
     const bool is_b = i >= fs.B_u;
-    float x[3] = {0.f, 0.f, 0.f};
-    float target = 0.f;
-    if (valid) {
-      draw_sample(md, i, fs.B_u, step, x);
-      target = sample_target(md, x);
-    }
-    // ---- encode -> fp16 h_0 row
-    {
-      float f[64];
+    const float target = valid ? samples[(size_t)m * Bs + i].w : 0.f;
+    // ---- level-major fp16 features -> canonical h_0 row (16 B = 8 columns per chunk)
+    for (int j = 0; j * 8 < net.LF; ++j) {
+      uint4 u = make_uint4(0u, 0u, 0u, 0u);
+      if (valid) {
+        if constexpr (F == 1) {
+          uint32_t w[4];
 #pragma unroll
-      for (int l = 0; l < kMaxLevels; ++l) {
-        if (l < net.L) {
-          float fl[F];
-          encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
-#pragma unroll
-          for (int j = 0; j < F; ++j)
-            if (l * F + j < 64) f[l * F + j] = fl[j];
+          for (int q = 0; q < 4; ++q) {
+            const unsigned short* p = reinterpret_cast<const unsigned short*>(featm);
+            uint32_t lo = p[(size_t)(8 * j + 2 * q) * Bs + i], hi = p[(size_t)(8 * j + 2 * q + 1) * Bs + i];
+            w[q] = lo | (hi << 16);
+          }
+          u = make_uint4(w[0], w[1], w[2], w[3]);
+        } else if constexpr (F == 2) {
+          const uint32_t* p = reinterpret_cast<const uint32_t*>(featm);
+          u = make_uint4(p[(size_t)(4 * j) * Bs + i], p[(size_t)(4 * j + 1) * Bs + i], p[(size_t)(4 * j + 2) * Bs + i],
+                         p[(size_t)(4 * j + 3) * Bs + i]);
+        } else if constexpr (F == 4) {
+          const uint2* p = reinterpret_cast<const uint2*>(featm);
+          uint2 a = p[(size_t)(2 * j) * Bs + i], b = p[(size_t)(2 * j + 1) * Bs + i];
+          u = make_uint4(a.x, a.y, b.x, b.y);
+        } else {
+          u = reinterpret_cast<const uint4*>(featm)[(size_t)j * Bs + i];
         }
       }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j * 8 < LF) st_row8(smem + lay.h[0], lay.h_sbo[0], t, j, f + 8 * j);
+      *reinterpret_cast<uint4*>(smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0] + j * 128) = u;
     }
     fence_async_smem();
     fence_before();
@@ -276,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitSca
 #pragma unroll
       for (int n = 0; n < 64; ++n) {
         float v = z[n] + bias[k * 64 + n];
-        bool pos = v > 0.f;
+        bool pos = v > 0.f && valid;
         if (n < 32) m0 |= (uint32_t)pos << n; else m1 |= (uint32_t)pos << (n - 32);
         z[n] = pos ? v : 0.f;
       }
@@ -345,7 +244,6 @@ __global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitSca
     __syncthreads();
 
     // ---- backward through the hidden layers
-    float dfeat[64];
     for (int k = H - 1; k >= 0; --k) {
       const int in = net.in_dim[k];
       if (t == 0) {
@@ -375,27 +273,28 @@ __global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitSca
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, t, j, dh + 8 * j);
-      } else {
+      } else if (valid) {
+        // dfeat, unscaled, level-major (coalesced across the tile)
 #pragma unroll
-        for (int n = 0; n < 64; ++n) dfeat[n] = dh[n] * inv_scale;
+        for (int c = 0; c < 64; c += F) {
+          if (c < net.LF) {
+            float* o = dfeatm + ((size_t)(c / F) * Bs + i) * F;
+            if constexpr (F == 1) { o[0] = dh[c] * inv_scale; }
+            else if constexpr (F == 2) { *reinterpret_cast<float2*>(o) = make_float2(dh[c] * inv_scale, dh[c + 1] * inv_scale); }
+            else {
+#pragma unroll
+              for (int q = 0; q < F; q += 4)
+                *reinterpret_cast<float4*>(o + q) = make_float4(dh[c + q] * inv_scale, dh[c + q + 1] * inv_scale,
+                                                                dh[c + q + 2] * inv_scale, dh[c + q + 3] * inv_scale);
+            }
+          }
+        }
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
     first = false;
-    // ---- table scatter-add
-    if (valid) {
-#pragma unroll
-      for (int l = 0; l < kMaxLevels; ++l) {
-        if (l < net.L) {
-          float df[F];
-#pragma unroll
-          for (int j = 0; j < F; ++j) df[j] = (l * F + j < 64) ? dfeat[l * F + j] : 0.f;
-          scatter_level<F>(G, GX, net.lv[l], net.table_mask, x, df);
-        }
-      }
-    }
   }
 
   // ---- flush the CTA's weight gradients (TMEM dW_k, smem dW_H) once
@@ -427,11 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2) fit_tc_kernel(GroupArgs g, FitSca
     for (int n = t; n < 64; n += kThreads) grad_add(G, GX, net.w_off[H] + n, red[n]);
     if (t == 0 && net.bias) grad_add(G, GX, net.b_off[H], red[64]);
   }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(lay.ncols));
+  mlp_teardown(tmem, lay);
 }
 
 // ============================================================ host side
@@ -493,7 +388,8 @@ static float loss_scale_for(int B_u) {
   return (float)(1 << e);
 }
 
-void launch_fit_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st) {
+void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const __half* feat, const float4* samples,
+                   float* dfeat, int Bs, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L)) return;
   const int total = fs.B_u + fs.B_b;
@@ -503,10 +399,10 @@ void launch_fit_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaSt
   dim3 grid(per_model, nmodels);
   float ls = loss_scale_for(fs.B_u);
   switch (g.net.F) {
-#define CASE_F(FF)                                                                                  \
-  case FF:                                                                                          \
-    cudaFuncSetAttribute(fit_tc_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
-    fit_tc_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls);                               \
+#define CASE_F(FF)                                                                                   \
+  case FF:                                                                                           \
+    cudaFuncSetAttribute(mlp_fit_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
+    mlp_fit_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls, feat, samples, dfeat, Bs);     \
     break;
     CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
 #undef CASE_F
@@ -528,32 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, co
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
-                 "r"(lay.ncols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  if (t == 0) {
-    mbar_init(mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int k = 0; k < H; ++k) {
-    const int in = net.in_dim[k];
-    const float* W = P + net.w_off[k];
-    for (int e = t; e < 64 * in; e += kThreads) {
-      int n = e / in, i = e - n * in;
-      *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) = __float2half_rn(W[e]);
-    }
-    for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
-  }
-  for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
-  if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
-  fence_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tslot;
+  const uint32_t tmem = mlp_setup(net, P, smem, lay, false);
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0;
   const long long ntiles = (q + kTileM - 1) / kTileM;
@@ -582,11 +453,10 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, co
     __syncthreads();
     float hH[64];
     for (int k = 0; k < H; ++k) {
-      const int in = net.in_dim[k];
       if (t == 0) {
         fence_after();
         gemm(tmem, smem_u32(smem + lay.h[k]), 128, lay.h_sbo[k], 256, smem_u32(smem + lay.w[k]), 128,
-             lay.w_sbo[k], 256, in / 16, make_idesc(128, 64, 0, 0), false);
+             lay.w_sbo[k], 256, net.in_dim[k] / 16, make_idesc(128, 64, 0, 0), false);
         mma_commit(mbar);
       }
       mbar_wait(mbar, phase);
@@ -614,11 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, co
     for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
     if (j < q) yout[j] = y;
   }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(lay.ncols));
+  mlp_teardown(tmem, lay);
 }
 
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,

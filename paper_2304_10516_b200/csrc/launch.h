@@ -54,9 +54,21 @@ void launch_debug_encode(const NetDesc& net, const float* P, const float* x01, l
 void launch_debug_forward_simt(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                                cudaStream_t st);
 
-// tensor-core (tcgen05) kernels — kernels_tc.cu
+// level-major fp16 fit pipeline — kernels_lm.cu (CUDA cores) + kernels_tc.cu (tcgen05)
+struct LmWorkspace {
+  float4* samples;   // [model][Bs] (x, y, z, target)
+  __half* feat;      // [model][level][Bs][F] fp16
+  float* dfeat;      // [model][level][Bs][F] fp32
+  int Bs;            // per-model sample stride
+};
+size_t lm_workspace_bytes(const NetDesc& net, int nmodels, int Bs);
+LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs);
+void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
+void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
+void launch_encode_bwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 bool tc_supported(const NetDesc& net);
-void launch_fit_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
+void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const __half* feat, const float4* samples,
+                   float* dfeat, int Bs, cudaStream_t st);
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
 
