@@ -249,6 +249,10 @@ INR_API inr_status inr_debug_forward(const inr_model* m, const float* x01, int64
  * "probe", "range".  inr_profile_enable(1) also clears previous records. */
 INR_API inr_status inr_profile_enable(int32_t on);
 INR_API inr_status inr_profile_read(const char* kernel, double* total_ms, int64_t* launches);
+/* Device time (ms) from the first recorded kernel start to the last recorded
+ * kernel end since inr_profile_enable(1) (same stream), i.e. the span of the
+ * timed work without host-side launch or graph-capture time. */
+INR_API inr_status inr_profile_span(double* span_ms);
 /* Number of kernels this library has launched since load (bench evidence). */
 INR_API int64_t inr_kernel_launches(void);
 

@@ -31,11 +31,23 @@ struct LevelInfo {
   int64_t offset;   // float offset of the level table in the parameter vector
 };
 
+constexpr int kMaxTensors = kMaxLevels + 2 * kMaxLayers;
+constexpr int kTensorAlign = 64;  // internal tensor offsets are multiples of 64 floats (256 B)
+
 // Per-configuration constants (same for every model of a group); passed by value.
+// Parameters are stored in the declared order (tables by level, then W_0, b_0,
+// ..., W_H, b_H) but every tensor starts at a 256-B aligned internal offset, so
+// an F = 2 entry pair {2k, 2k+1} is one 16-B aligned vector (paired corners).
 struct NetDesc {
   int L, F, H, LF, D, bias;
   uint32_t table_mask;              // T - 1
-  int64_t nparams;
+  int64_t nparams;                  // internal (padded) parameter count
+  int64_t ndecl;                    // declared parameter count
+  int ntensors;
+  int64_t t_off[kMaxTensors];       // internal offset of tensor t
+  int64_t t_decl[kMaxTensors];      // declared offset of tensor t
+  int64_t t_len[kMaxTensors];
+  int t_fan_in[kMaxTensors];        // 0: table, > 0: weight matrix (He-uniform), -1: bias
   int64_t w_off[kMaxLayers];        // float offset of W_k (row-major [out][in])
   int64_t b_off[kMaxLayers];        // float offset of b_k (or -1)
   int in_dim[kMaxLayers], out_dim[kMaxLayers];
@@ -186,6 +198,10 @@ __device__ __forceinline__ FVec<F> load_entry(const float* __restrict__ p) {
 }
 
 // Encode one level: feat[f] = sum_c w_c theta[idx_c][f] (summed in corner order).
+// The two x-neighbour corners (c, c+1) of a cell land in one aligned entry pair
+// {2k, 2k+1} whenever idx_c ^ idx_{c+1} == 1 (always for even x on hashed
+// levels, since h(x+1) = h(x) ^ 1 there; for even idx on dense levels): then one
+// 16-B (F = 2) or 8-B (F = 1) load fetches both.
 template <int F>
 __device__ __forceinline__ void encode_level(const float* __restrict__ params, const LevelInfo& lv, uint32_t mask,
                                              const float x[3], float feat[F]) {
@@ -194,12 +210,32 @@ __device__ __forceinline__ void encode_level(const float* __restrict__ params, c
 #pragma unroll
   for (int f = 0; f < F; ++f) feat[f] = 0.f;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint32_t idx = corner_index(cell, c, lv, mask);
-    float w = corner_weight(cell, c);
-    FVec<F> e = load_entry<F>(tab + (size_t)idx * F);
+  for (int c = 0; c < 8; c += 2) {
+    const uint32_t i0 = corner_index(cell, c, lv, mask), i1 = corner_index(cell, c + 1, lv, mask);
+    const float w0 = corner_weight(cell, c), w1 = corner_weight(cell, c + 1);
+    FVec<F> e0, e1;
+    if constexpr (F <= 2) {
+      if ((i0 ^ i1) == 1u) {
+        const uint32_t lo = min(i0, i1);
+        FVec<2 * F> pr = load_entry<2 * F>(tab + (size_t)lo * F);
+        const bool swap = i0 > i1;
 #pragma unroll
-    for (int f = 0; f < F; ++f) feat[f] = fmaf(w, e.v[f], feat[f]);
+        for (int f = 0; f < F; ++f) {
+          e0.v[f] = swap ? pr.v[F + f] : pr.v[f];
+          e1.v[f] = swap ? pr.v[f] : pr.v[F + f];
+        }
+      } else {
+        e0 = load_entry<F>(tab + (size_t)i0 * F);
+        e1 = load_entry<F>(tab + (size_t)i1 * F);
+      }
+    } else {
+      e0 = load_entry<F>(tab + (size_t)i0 * F);
+      e1 = load_entry<F>(tab + (size_t)i1 * F);
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) feat[f] = fmaf(w0, e0.v[f], feat[f]);
+#pragma unroll
+    for (int f = 0; f < F; ++f) feat[f] = fmaf(w1, e1.v[f], feat[f]);
   }
 }
 
@@ -217,20 +253,48 @@ __device__ __forceinline__ void scatter_level(float* __restrict__ grads, unsigne
                                               const float dfeat[F]) {
   Cell cell = level_cell(x, lv.res);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint32_t idx = corner_index(cell, c, lv, mask);
-    float w = corner_weight(cell, c);
-    size_t off = (size_t)lv.offset + (size_t)idx * F;
+  for (int c = 0; c < 8; c += 2) {
+    const uint32_t i0 = corner_index(cell, c, lv, mask), i1 = corner_index(cell, c + 1, lv, mask);
+    const float w0 = corner_weight(cell, c), w1 = corner_weight(cell, c + 1);
     if (gfx) {
 #pragma unroll
-      for (int f = 0; f < F; ++f) red_add_fx(gfx + off + f, w * dfeat[f]);
-    } else if constexpr (F == 2) {
-      atomicAdd(reinterpret_cast<float2*>(grads + off), make_float2(w * dfeat[0], w * dfeat[1]));
+      for (int f = 0; f < F; ++f) {
+        red_add_fx(gfx + (size_t)lv.offset + (size_t)i0 * F + f, w0 * dfeat[f]);
+        red_add_fx(gfx + (size_t)lv.offset + (size_t)i1 * F + f, w1 * dfeat[f]);
+      }
+      continue;
+    }
+    float* base = grads + lv.offset;
+    if constexpr (F == 2) {
+      if ((i0 ^ i1) == 1u) {  // both corners in one aligned 16-B entry pair: one vector red
+        const bool swap = i0 > i1;
+        const float wl = swap ? w1 : w0, wh = swap ? w0 : w1;
+        atomicAdd(reinterpret_cast<float4*>(base + (size_t)min(i0, i1) * 2),
+                  make_float4(wl * dfeat[0], wl * dfeat[1], wh * dfeat[0], wh * dfeat[1]));
+      } else {
+        atomicAdd(reinterpret_cast<float2*>(base + (size_t)i0 * 2), make_float2(w0 * dfeat[0], w0 * dfeat[1]));
+        atomicAdd(reinterpret_cast<float2*>(base + (size_t)i1 * 2), make_float2(w1 * dfeat[0], w1 * dfeat[1]));
+      }
+    } else if constexpr (F == 1) {
+      if ((i0 ^ i1) == 1u) {
+        const bool swap = i0 > i1;
+        atomicAdd(reinterpret_cast<float2*>(base + min(i0, i1)),
+                  swap ? make_float2(w1 * dfeat[0], w0 * dfeat[0]) : make_float2(w0 * dfeat[0], w1 * dfeat[0]));
+      } else {
+        atomicAdd(base + i0, w0 * dfeat[0]);
+        atomicAdd(base + i1, w1 * dfeat[0]);
+      }
     } else if constexpr (F == 4) {
-      atomicAdd(reinterpret_cast<float4*>(grads + off), make_float4(w * dfeat[0], w * dfeat[1], w * dfeat[2], w * dfeat[3]));
+      atomicAdd(reinterpret_cast<float4*>(base + (size_t)i0 * 4), make_float4(w0 * dfeat[0], w0 * dfeat[1], w0 * dfeat[2], w0 * dfeat[3]));
+      atomicAdd(reinterpret_cast<float4*>(base + (size_t)i1 * 4), make_float4(w1 * dfeat[0], w1 * dfeat[1], w1 * dfeat[2], w1 * dfeat[3]));
     } else {
 #pragma unroll
-      for (int f = 0; f < F; ++f) red_add(grads + off + f, w * dfeat[f]);
+      for (int q = 0; q < F; q += 4) {
+        atomicAdd(reinterpret_cast<float4*>(base + (size_t)i0 * F + q),
+                  make_float4(w0 * dfeat[q], w0 * dfeat[q + 1], w0 * dfeat[q + 2], w0 * dfeat[q + 3]));
+        atomicAdd(reinterpret_cast<float4*>(base + (size_t)i1 * F + q),
+                  make_float4(w1 * dfeat[q], w1 * dfeat[q + 1], w1 * dfeat[q + 2], w1 * dfeat[q + 3]));
+      }
     }
   }
 }

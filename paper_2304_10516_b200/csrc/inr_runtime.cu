@@ -76,17 +76,25 @@ static cudaEvent_t prof_event() {
 }
 
 // Brackets one kernel launch with events on its stream when profiling is on.
+// (inside a stream capture the records must be "external" to become event nodes)
+static void prof_record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else cudaEventRecord(e, st);
+}
+
 struct ProfScope {
   int kind;
   cudaStream_t st;
   cudaEvent_t a = nullptr;
   ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
-    if (g_prof_on) { a = prof_event(); cudaEventRecord(a, st); }
+    if (g_prof_on) { a = prof_event(); prof_record(a, st); }
   }
   ~ProfScope() {
     if (a) {
       cudaEvent_t b = prof_event();
-      cudaEventRecord(b, st);
+      prof_record(b, st);
       g_prof.push_back({kind, a, b});
     }
   }
@@ -100,6 +108,17 @@ static void prof_clear() {
 extern "C" inr_status inr_profile_enable(int32_t on) {
   g_prof_on = on != 0;
   if (g_prof_on) prof_clear();
+  return INR_OK;
+}
+
+extern "C" inr_status inr_profile_span(double* span_ms) {
+  if (!span_ms) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *span_ms = 0;
+  if (g_prof.empty()) return INR_OK;
+  CK(cudaEventSynchronize(g_prof.back().b));
+  float t = 0;
+  CK(cudaEventElapsedTime(&t, g_prof.front().a, g_prof.back().b));
+  *span_ms = t;
   return INR_OK;
 }
 
@@ -131,8 +150,8 @@ struct inr_model {
   inr_block blk;
   int device;
   NetDesc net;
-  int64_t P;            // parameters
-  int64_t P_pad;        // padded stride of each array
+  int64_t P;            // declared parameters (API)
+  int64_t P_pad;        // internal (aligned, padded) length of each array
   void* mem = nullptr;
   float* params = nullptr;
   float* grads = nullptr;
@@ -205,7 +224,18 @@ static void build_net(const inr_config& c, NetDesc& net) {
   net.bias = c.mlp_bias ? 1 : 0;
   uint64_t T = 1ull << c.log2_table_size;
   net.table_mask = (uint32_t)(T - 1);
-  int64_t off = 0;
+  int64_t off = 0, decl = 0;
+  auto add_tensor = [&](int64_t len, int fan_in) {
+    off = (off + kTensorAlign - 1) / kTensorAlign * kTensorAlign;
+    int t = net.ntensors++;
+    net.t_off[t] = off;
+    net.t_decl[t] = decl;
+    net.t_len[t] = len;
+    net.t_fan_in[t] = fan_in;
+    off += len;
+    decl += len;
+    return net.t_off[t];
+  };
   for (int l = 0; l < c.levels; ++l) {
     double r = std::floor((double)c.base_resolution * std::pow((double)c.per_level_scale, (double)l));
     uint64_t res = (uint64_t)r;
@@ -214,18 +244,16 @@ static void build_net(const inr_config& c, NetDesc& net) {
     lv.res = (uint32_t)res;
     if (dense <= (double)T) { lv.size = (uint32_t)((res + 1) * (res + 1) * (res + 1)); lv.dense = 1; }
     else { lv.size = (uint32_t)T; lv.dense = 0; }
-    lv.offset = off;
-    off += (int64_t)lv.size * c.features;
+    lv.offset = add_tensor((int64_t)lv.size * c.features, 0);
   }
   for (int k = 0; k <= net.H; ++k) {
     net.in_dim[k] = k == 0 ? net.LF : kWidth;
     net.out_dim[k] = k == net.H ? net.D : kWidth;
-    net.w_off[k] = off;
-    off += (int64_t)net.in_dim[k] * net.out_dim[k];
-    net.b_off[k] = -1;
-    if (net.bias) { net.b_off[k] = off; off += net.out_dim[k]; }
+    net.w_off[k] = add_tensor((int64_t)net.in_dim[k] * net.out_dim[k], net.in_dim[k]);
+    net.b_off[k] = net.bias ? add_tensor(net.out_dim[k], -1) : -1;
   }
-  net.nparams = off;
+  net.nparams = (off + kTensorAlign - 1) / kTensorAlign * kTensorAlign;
+  net.ndecl = decl;
 }
 
 static void philox_key(uint64_t seed, uint32_t stream, uint32_t& k0, uint32_t& k1) {
@@ -247,8 +275,8 @@ static void block_geometry(inr_model* m) {
 
 // frozen: parameters only; host_only: no device parameter buffer (staged lazily on decode).
 static inr_status alloc_model(inr_model* m, bool frozen, bool host_only = false) {
-  m->P = m->net.nparams;
-  m->P_pad = (m->P + 63) / 64 * 64;
+  m->P = m->net.ndecl;
+  m->P_pad = m->net.nparams;
   size_t bytes = (size_t)m->P_pad * sizeof(float) * (host_only ? 0 : (frozen ? 1 : 4)) + 256;
   if (!frozen && m->cfg.reduction == INR_REDUCE_DETERMINISTIC) bytes += (size_t)m->P_pad * 8;
   CK(cudaMalloc(&m->mem, bytes));
@@ -368,7 +396,7 @@ static inr_status ensure_device_params(const inr_model* cm, cudaStream_t st) {
   inr_model* m = const_cast<inr_model*>(cm);
   if (!m->host_resident || m->staged) return INR_OK;
   if (!m->params) CK(cudaMalloc((void**)&m->params, (size_t)m->P_pad * 4));
-  CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P_pad * 4, cudaMemcpyHostToDevice, st));
   m->staged = true;
   return INR_OK;
 }
@@ -512,14 +540,17 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   } ws_free{ws_mem, st};
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
   const int launches_per_step = (tc ? 6 : 3) * nchunks;
-  // Replay a captured step when there are enough steps to amortize capture and
-  // the stream is capturable (not the legacy default stream).
+  // CUDA graphs (launch-gap free): without probing, capture one step and replay it
+  // per step; while profiling, capture the whole loop (with its event records)
+  // once, so per-kernel timings come from the same graph execution.
   cudaGraphExec_t exec = nullptr;
-  if (steps >= 4 && st != nullptr && !g_prof_on) {
+  const bool graphs = st != nullptr && !probing && steps >= 2;
+  const bool whole = graphs && g_prof_on;
+  if (graphs) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     long long before = g_launches.load();
-    enqueue_step(st);
+    for (int s = 0; s < (whole ? steps : 1); ++s) enqueue_step(st);
     g_launches.store(before);  // captured launches are counted per replay below
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
@@ -533,9 +564,10 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   std::vector<int> reached(nmodels, 0);
   for (int s = 0; s < steps; ++s) {
     if (exec) {
+      if (whole && s > 0) { taken = s + 1; continue; }
       cudaError_t e = cudaGraphLaunch(exec, st);
       if (e != cudaSuccess) { cudaGraphExecDestroy(exec); return cuda_fail(e, "cudaGraphLaunch"); }
-      count_launch(launches_per_step);
+      count_launch((long long)launches_per_step * (whole ? steps : 1));
     } else {
       enqueue_step(st);
       CK_LAUNCH("fit step");
@@ -698,21 +730,32 @@ extern "C" inr_status inr_value_range(const inr_view* v, float* minmax, cudaStre
 }
 
 // ------------------------------------------------------------ parity surface
+// internal (aligned) device layout <-> declared (contiguous) host layout
+static inr_status copy_tensors(const NetDesc& net, float* dst, const float* src, cudaMemcpyKind kind) {
+  for (int t = 0; t < net.ntensors; ++t) {
+    if (kind == cudaMemcpyDeviceToHost)
+      CK(cudaMemcpy(dst + net.t_decl[t], src + net.t_off[t], (size_t)net.t_len[t] * 4, kind));
+    else if (kind == cudaMemcpyHostToDevice)
+      CK(cudaMemcpy(dst + net.t_off[t], src + net.t_decl[t], (size_t)net.t_len[t] * 4, kind));
+    else  // host internal -> host declared
+      memcpy(dst + net.t_decl[t], src + net.t_off[t], (size_t)net.t_len[t] * 4);
+  }
+  return INR_OK;
+}
+
 static inr_status copy_out(const inr_model* m, const float* src, float* host, int64_t n) {
   if (!m || !host) return fail(INR_ERR_INVALID_ARG, "NULL argument");
   if (n != m->P) return fail(INR_ERR_INVALID_ARG, "n must equal inr_param_count (%lld)", (long long)m->P);
   if (!src) return fail(INR_ERR_STATE, "this state does not exist on a frozen snapshot");
   CK(cudaSetDevice(m->device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(host, src, (size_t)n * 4, cudaMemcpyDeviceToHost));
-  return INR_OK;
+  return copy_tensors(m->net, host, src, cudaMemcpyDeviceToHost);
 }
 
 extern "C" inr_status inr_get_params(const inr_model* m, float* host, int64_t n) {
   if (m && m->host_resident && !m->staged) {
     if (!host || n != m->P) return fail(INR_ERR_INVALID_ARG, "bad arguments");
-    memcpy(host, m->host_params, (size_t)n * 4);
-    return INR_OK;
+    return copy_tensors(m->net, host, m->host_params, cudaMemcpyHostToHost);
   }
   return copy_out(m, m ? m->params : nullptr, host, n);
 }
@@ -730,8 +773,7 @@ extern "C" inr_status inr_set_params(inr_model* m, const float* host, int64_t n)
   if (n != m->P) return fail(INR_ERR_INVALID_ARG, "n must equal inr_param_count (%lld)", (long long)m->P);
   CK(cudaSetDevice(m->device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(m->params, host, (size_t)n * 4, cudaMemcpyHostToDevice));
-  return INR_OK;
+  return copy_tensors(m->net, m->params, host, cudaMemcpyHostToDevice);
 }
 
 extern "C" inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_t q, uint32_t* idx, float* feat,
@@ -850,16 +892,16 @@ extern "C" inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* co
     if (s) { delete m; for (auto* x : slot.models) inr_destroy(x); return s; }
     if (c->host_resident) {
       // "the learned neural network parameters are cached in system RAM"
-      cudaError_t e = cudaMallocHost((void**)&m->host_params, (size_t)m->P * 4);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(m->host_params, src->params, (size_t)m->P * 4, cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaMallocHost((void**)&m->host_params, (size_t)m->P_pad * 4);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(m->host_params, src->params, (size_t)m->P_pad * 4, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2H"); }
       m->host_resident = true;
       m->staged = false;
     } else {
-      cudaError_t e = cudaMemcpyAsync(m->params, src->params, (size_t)m->P * 4, cudaMemcpyDeviceToDevice, st);
+      cudaError_t e = cudaMemcpyAsync(m->params, src->params, (size_t)m->P_pad * 4, cudaMemcpyDeviceToDevice, st);
       if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2D"); }
     }
-    c->bytes += m->P * 4;
+    c->bytes += m->P * 4;  // stored parameter bytes (declared count)
     slot.models.push_back(m);
     slot.cmodels.push_back(m);
   }

@@ -21,25 +21,22 @@ constexpr int kLd = kTile + 1;   // smem row stride (bank-conflict-free column a
 // u01(Philox(key(seed, 0), (j, block_id, 0, 0)).x) (R14).
 __global__ void init_params_kernel(NetDesc net, float* __restrict__ params, uint32_t k0, uint32_t k1,
                                    uint32_t block_id) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < net.nparams;
-       j += (long long)gridDim.x * blockDim.x) {
-    double a = -1.0;  // -1: zero (bias)
-    if (j < net.w_off[0]) {
-      a = 1e-4;
-    } else {
-      for (int k = 0; k <= net.H; ++k) {
-        long long w0 = net.w_off[k], w1 = w0 + (long long)net.in_dim[k] * net.out_dim[k];
-        if (j >= w0 && j < w1) { a = sqrt(6.0 / (double)net.in_dim[k]); break; }
-      }
-    }
-    float v = 0.f;
-    if (a > 0) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < net.nparams;
+       p += (long long)gridDim.x * blockDim.x) {
+    float v = 0.f;  // padding and biases
+    for (int t = 0; t < net.ntensors; ++t) {
+      if (p < net.t_off[t] || p >= net.t_off[t] + net.t_len[t]) continue;
+      const int fan = net.t_fan_in[t];
+      if (fan < 0) break;
+      const long long j = net.t_decl[t] + (p - net.t_off[t]);   // declared index: the Philox counter
+      const double a = fan == 0 ? 1e-4 : sqrt(6.0 / (double)fan);
       U4 u = philox((uint32_t)j, block_id, 0u, 0u, k0, k1);
       double U = (double)(u.x >> 8) * 5.9604644775390625e-08;
       double lo = -a, hi = a;
       v = __double2float_rn(__dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), U)));
+      break;
     }
-    params[j] = v;
+    params[p] = v;
   }
 }
 

@@ -100,6 +100,7 @@ _SIG = {
     "inr_kernel_launches": (_I64, []),
     "inr_profile_enable": (_I32, [_I32]),
     "inr_profile_read": (_I32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
+    "inr_profile_span": (_I32, [ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIG.items():
     _f = getattr(_lib, _name)
@@ -299,3 +300,10 @@ def inr_profile_read(kernel):
     ms, n = ctypes.c_double(), _I64()
     _check(_lib.inr_profile_read(kernel.encode(), ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def inr_profile_span():
+    """Device ms from the first recorded kernel start to the last kernel end."""
+    ms = ctypes.c_double()
+    _check(_lib.inr_profile_span(ctypes.byref(ms)))
+    return ms.value
