@@ -282,8 +282,24 @@ def run_ours(args):
     dec_ms = dnr.allreduce_max(e0.elapsed_time(e1))
     inr.inr_profile_enable(0)
     vox_local = BLOCK ** 3 * len(d.models)
+    # random queries over the rank's blocks (bucketed by block, tensor-core MLP for fp16 models)
+    nq = 1 << 22
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    pts = torch.rand((nq, 3), device=dev, generator=g, dtype=torch.float32)
+    span = torch.tensor([d.hi[0] - d.lo[0], d.hi[1] - d.lo[1], d.hi[2] - d.lo[2]], device=dev, dtype=torch.float32)
+    pts = pts * span + torch.tensor(d.lo, device=dev, dtype=torch.float32)
+    qout = torch.empty(nq, device=dev)
+    inr.inr_decode_group(d.models, pts.data_ptr(), nq, qout.data_ptr(), 0, stream)   # warm
+    torch.cuda.synchronize()
+    e0.record()
+    inr.inr_decode_group(d.models, pts.data_ptr(), nq, qout.data_ptr(), 0, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    q_ms = dnr.allreduce_max(e0.elapsed_time(e1))
     decode = {"voxels_per_s": vox_local * world / (dec_ms / 1e3), "ms": dec_ms, "voxels": vox_local * world,
-              "kernel": "decode_grid (fp32 CUDA-core MLP)"}
+              "kernel": "decode_grid: " + ("tcgen05 fp16 MLP, R19 vertex elision" if prec else "fp32 CUDA-core MLP"),
+              "queries_per_s": nq * world / (q_ms / 1e3), "queries": nq * world, "query_ms": q_ms}
     done = args.warmup + args.steps + e_steps
     if args.psnr_steps > done:
         d.fit(vol, args.psnr_steps - done, B_U, opts, stream, report=True)

@@ -239,6 +239,24 @@ __device__ __forceinline__ void encode_level(const float* __restrict__ params, c
   }
 }
 
+// Inference variant (decode): when the position is a lattice vertex of this level
+// (all three fractional weights are 0, e.g. x = j/R with N_l >= R, DESIGN R19)
+// only corner 0 has a non-zero weight, and it is 1: fetch that one entry.  The
+// skipped corners have weight exactly 0, so for finite tables the result is
+// bitwise the 8-corner sum (fma(0, v, acc) == acc).
+template <int F>
+__device__ __forceinline__ void encode_level_infer(const float* __restrict__ params, const LevelInfo& lv,
+                                                   uint32_t mask, const float x[3], float feat[F]) {
+  Cell cell = level_cell(x, lv.res);
+  if (cell.w[0] == 0.f && cell.w[1] == 0.f && cell.w[2] == 0.f) {
+    FVec<F> e = load_entry<F>(params + lv.offset + (size_t)corner_index(cell, 0, lv, mask) * F);
+#pragma unroll
+    for (int f = 0; f < F; ++f) feat[f] = fmaf(1.f, e.v[f], 0.f);
+    return;
+  }
+  encode_level<F>(params, lv, mask, x, feat);
+}
+
 // Scatter-add of one level's gradient: dtheta[idx_c][f] += w_c dfeat[f].
 __device__ __forceinline__ void red_add(float* p, float v) { atomicAdd(p, v); }
 

@@ -646,7 +646,11 @@ extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], 
   else { os[0] = 1; os[1] = res[0]; os[2] = (long long)res[0] * res[1]; }
   int r[3] = {res[0], res[1], res[2]};
   ModelDev md = model_dev(m);
-  { ProfScope p(PK_DECODE_GRID, st); launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st); }
+  {
+    ProfScope p(PK_DECODE_GRID, st);
+    if (m->cfg.precision == INR_PREC_FP16_MLP) launch_decode_grid_tc(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
+    else launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
+  }
   CK_LAUNCH("decode_grid");
   return INR_OK;
 }
@@ -694,7 +698,25 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
     if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int), st);
     if (e != cudaSuccess) { delete qa; return cuda_fail(e, "strict flag"); }
   }
-  if (q > 0) { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_simt(*qa, xyz, q, out, dflag, st); }
+  qa->nmodels = nmodels;
+  if (q > 0 && m0->cfg.precision == INR_PREC_FP16_MLP) {
+    // tensor-core path: bucket the queries by block, then 128-query tiles of one block each
+    void* ws = nullptr;
+    cudaError_t e = cudaMallocAsync(&ws, query_workspace_bytes(q, nmodels), st);
+    if (e != cudaSuccess) { delete qa; return cuda_fail(e, "query workspace"); }
+    QueryBuckets qb;
+    launch_query_buckets(*qa, xyz, q, out, dflag, ws, qb, st);
+    GroupArgs* g = new GroupArgs();
+    g->net = qa->net;
+    g->nmodels = nmodels;
+    for (int i = 0; i < nmodels; ++i) g->md[i] = qa->md[i];
+    { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_tc(*g, xyz, q, out, qb.perm, qb.tile_slot, qb.ntiles, st); }
+    delete g;
+    cudaFreeAsync(ws, st);
+  } else if (q > 0) {
+    ProfScope p(PK_DECODE_QUERY, st);
+    launch_decode_query_simt(*qa, xyz, q, out, dflag, st);
+  }
   delete qa;
   CK_LAUNCH("decode_query");
   if (strict) {

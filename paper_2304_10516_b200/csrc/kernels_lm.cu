@@ -129,6 +129,82 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
   }
 }
 
+// ------------------------------------------------------- query bucketing
+// Decode queries on tensor cores need every 128-query tile to come from one
+// block: route each query to its block (R5), count per block, lay the blocks'
+// buckets out padded to 128, scatter query indices into them.  Bucket order is
+// not deterministic, but each query's value does not depend on its tile slot.
+__global__ void route_kernel(QueryArgs qa, const float* __restrict__ xyz, long long q, int* __restrict__ slot_of,
+                             int* __restrict__ counts, int* __restrict__ dflag, float* __restrict__ out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  int bc[3];
+  bool outside = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const float p = __ldg(xyz + 3 * j + d);
+    outside |= !(p >= 0.f && p <= (float)(qa.N[d] - 1));
+    const int b = (int)floorf(__fdiv_rn(p, (float)qa.n[d]));
+    bc[d] = min(max(b, 0), qa.B[d] - 1);
+  }
+  const int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
+  const int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
+  slot_of[j] = slot;
+  if (slot >= 0) atomicAdd(counts + slot, 1);
+  else out[j] = __int_as_float(0x7fc00000);
+  if (outside && dflag) atomicOr(dflag, 1);
+}
+
+__global__ void bucket_offsets_kernel(const int* __restrict__ counts, int nmodels, int* __restrict__ offsets,
+                                      int* __restrict__ tile_slot, int* __restrict__ ntiles) {
+  __shared__ int off[kMaxGroup + 1];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < nmodels; ++s) { off[s] = o; o += (counts[s] + 127) / 128 * 128; }
+    off[nmodels] = o;
+    *ntiles = o / 128;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < nmodels; s += blockDim.x) offsets[s] = off[s];
+  for (int s = 0; s < nmodels; ++s)
+    for (int tt = off[s] / 128 + threadIdx.x; tt < off[s + 1] / 128; tt += blockDim.x) tile_slot[tt] = s;
+}
+
+__global__ void bucket_scatter_kernel(const int* __restrict__ slot_of, long long q, const int* __restrict__ offsets,
+                                      int* __restrict__ cursor, int* __restrict__ perm) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= q) return;
+  const int s = slot_of[j];
+  if (s < 0) return;
+  perm[offsets[s] + atomicAdd(cursor + s, 1)] = (int)j;
+}
+
+size_t query_workspace_bytes(long long q, int nmodels) {
+  return (size_t)q * 4 + (size_t)(q + 128ll * nmodels) * 4 + 3 * 4 * kMaxGroup + (size_t)(q / 128 + nmodels + 2) * 4 +
+         6 * 256;
+}
+
+void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag, void* ws,
+                          QueryBuckets& b, cudaStream_t st) {
+  char* p = (char*)ws;
+  auto take = [&](size_t bytes) { char* r = p; p += (bytes + 255) / 256 * 256; return r; };
+  int* slot_of = (int*)take((size_t)q * 4);
+  b.perm = (int*)take((size_t)(q + 128ll * qa_nmodels(qa)) * 4);
+  int* counts = (int*)take(4 * kMaxGroup);
+  int* offsets = (int*)take(4 * kMaxGroup);
+  int* cursor = (int*)take(4 * kMaxGroup);
+  b.tile_slot = (int*)take((size_t)(q / 128 + qa_nmodels(qa) + 2) * 4);
+  b.ntiles = (int*)take(4);
+  cudaMemsetAsync(counts, 0, 4 * kMaxGroup, st);
+  cudaMemsetAsync(cursor, 0, 4 * kMaxGroup, st);
+  cudaMemsetAsync(b.perm, 0xff, (size_t)(q + 128ll * qa_nmodels(qa)) * 4, st);
+  const unsigned grid = (unsigned)((q + 255) / 256);
+  route_kernel<<<grid, 256, 0, st>>>(qa, xyz, q, slot_of, counts, dflag, out);
+  bucket_offsets_kernel<<<1, 128, 0, st>>>(counts, qa_nmodels(qa), offsets, b.tile_slot, b.ntiles);
+  bucket_scatter_kernel<<<grid, 256, 0, st>>>(slot_of, q, offsets, cursor, b.perm);
+  count_launch(3);
+}
+
 // ============================================================ host launchers
 #define LM_DISPATCH_F(F_, ...)                           \
   switch (F_) {                                          \

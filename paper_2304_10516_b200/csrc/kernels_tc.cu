@@ -330,10 +330,12 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
 }
 
 // ============================================================ host side
-static bool build_layout(const NetDesc& net, Layout& L) {
+// train: the fit layout (ones groups, dz tile, dW accumulators in TMEM);
+// otherwise the forward-only layout (64 TMEM columns).
+static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   memset(&L, 0, sizeof L);
   if (net.LF % 16 != 0 || net.LF > 64 || net.H < 1 || net.H > kMaxLayers - 1 || net.D != 1) return false;
-  L.ones = net.bias ? 8 : 0;
+  L.ones = (net.bias && train) ? 8 : 0;
   uint32_t off = 0;
   auto take = [&](uint32_t bytes, uint32_t align) {
     off = (off + align - 1) / align * align;
@@ -349,7 +351,7 @@ static bool build_layout(const NetDesc& net, Layout& L) {
     L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
   }
   L.dz_sbo = 8 * 128;
-  L.dz = take(kTileM * 64 * 2, 1024);
+  if (train) L.dz = take(kTileM * 64 * 2, 1024);
   L.bias = take(net.H * 64 * 4, 16);
   L.wout = take(65 * 4, 16);
   L.red = take(66 * 4, 16);
@@ -358,11 +360,13 @@ static bool build_layout(const NetDesc& net, Layout& L) {
   // TMEM: [0, 64) layer accumulator; then dW_k (M = 64 rows, in_k + ones columns)
   // (8-column granularity; the last region is padded so 16-column loads stay inside)
   uint32_t col = 64;
-  for (int k = 0; k < net.H; ++k) {
-    L.col_dw[k] = col;
-    col += (uint32_t)(net.in_dim[k] + L.ones);
+  if (train) {
+    for (int k = 0; k < net.H; ++k) {
+      L.col_dw[k] = col;
+      col += (uint32_t)(net.in_dim[k] + L.ones);
+    }
+    col = std::max(col, L.col_dw[net.H - 1] + (uint32_t)((net.in_dim[net.H - 1] + L.ones + 15) / 16 * 16));
   }
-  col = std::max(col, L.col_dw[net.H - 1] + (uint32_t)((net.in_dim[net.H - 1] + L.ones + 15) / 16 * 16));
   if (col > 512) return false;
   L.ncols = 32;
   while (L.ncols < col) L.ncols <<= 1;
@@ -412,33 +416,103 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
 }
 
 // ------------------------------------------------------------ forward only
-// Network output for block-normalized coordinates with the same tensor-core
-// forward as the fit kernel (debug / parity surface).
-template <int F>
-__global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, const float* __restrict__ P,
-                                                                const float* __restrict__ x01, long long q,
-                                                                float* __restrict__ yout, Layout lay) {
+// Network inference on tensor cores for 128-point tiles (same forward as the fit):
+//   MODE 0  debug: block-normalized x01[q] -> y[q] (normalized units)
+//   MODE 1  decode grid: x_j = fl32(j / R) lattice of one block, denormalized
+//           strided stores, optional fused SSE against ref (R18, R19)
+//   MODE 2  decode query: tiles of bucket-sorted query indices, every tile from
+//           one block (see the bucketing kernels below), x = fl32(fl32(p-o)/n)
+struct FwdArgs {
+  const float* x01;
+  float* y;
+  long long q;
+  int res[3];
+  float* out;
+  long long os[3];
+  const float* ref;
+  double* sse;
+  const float* xyz;
+  const int* perm;
+  const int* tile_slot;
+  const int* ntiles_dev;
+};
+
+template <int F, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int t = threadIdx.x, warp = t >> 5;
+  const NetDesc& net = g.net;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int H = net.H, LF = net.LF;
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  const uint32_t tmem = mlp_setup(net, P, smem, lay, false);
+  int cur = MODE == 2 ? -1 : 0;  // model whose weights are in smem
+  const uint32_t tmem = mlp_setup(net, g.md[0].params, smem, lay, false);
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0;
-  const long long ntiles = (q + kTileM - 1) / kTileM;
+  long long ntiles;
+  if constexpr (MODE == 0) ntiles = (a.q + kTileM - 1) / kTileM;
+  else if constexpr (MODE == 1) ntiles = ((long long)a.res[0] * a.res[1] * a.res[2] + kTileM - 1) / kTileM;
+  else ntiles = *a.ntiles_dev;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    int slot = 0;
+    if constexpr (MODE == 2) {
+      slot = a.tile_slot[tile];
+      if (slot != cur) {  // reload this block's weights (tiles are grouped by block)
+        __syncthreads();
+        const float* P = g.md[slot].params;
+        for (int k = 0; k < H; ++k) {
+          const int in = net.in_dim[k];
+          for (int e = t; e < 64 * in; e += kThreads) {
+            int n = e / in, i = e - n * in;
+            *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) =
+                __float2half_rn(P[net.w_off[k] + e]);
+          }
+          for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
+        }
+        for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
+        if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
+        cur = slot;
+      }
+    }
+    const ModelDev& md = g.md[slot];
+    const float* P = md.params;
     const long long j = tile * kTileM + t;
+    bool valid;
     float x[3] = {0.f, 0.f, 0.f};
-    if (j < q) { x[0] = __ldg(x01 + 3 * j); x[1] = __ldg(x01 + 3 * j + 1); x[2] = __ldg(x01 + 3 * j + 2); }
+    long long dst = 0;
+    if constexpr (MODE == 0) {
+      valid = j < a.q;
+      if (valid) { x[0] = __ldg(a.x01 + 3 * j); x[1] = __ldg(a.x01 + 3 * j + 1); x[2] = __ldg(a.x01 + 3 * j + 2); }
+    } else if constexpr (MODE == 1) {
+      valid = j < (long long)a.res[0] * a.res[1] * a.res[2];
+      if (valid) {
+        const int jx = (int)(j % a.res[0]);
+        const long long r = j / a.res[0];
+        const int jy = (int)(r % a.res[1]), jz = (int)(r / a.res[1]);
+        x[0] = __fdiv_rn((float)jx, (float)a.res[0]);
+        x[1] = __fdiv_rn((float)jy, (float)a.res[1]);
+        x[2] = __fdiv_rn((float)jz, (float)a.res[2]);
+        dst = jx * a.os[0] + jy * a.os[1] + jz * a.os[2];
+      }
+    } else {
+      const int qi = a.perm[j];
+      valid = qi >= 0;
+      if (valid) {
+        dst = qi;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          x[d] = __fdiv_rn(__fsub_rn(__ldg(a.xyz + 3 * (long long)qi + d), (float)md.o[d]), (float)md.n[d]);
+      }
+    }
     {
       float f[64];
 #pragma unroll
       for (int l = 0; l < kMaxLevels; ++l) {
         if (l < net.L) {
           float fl[F];
-          encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+          if (MODE == 0) encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+          else encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
 #pragma unroll
           for (int jj = 0; jj < F; ++jj)
             if (l * F + jj < 64) f[l * F + jj] = fl[jj];
@@ -467,7 +541,13 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, co
       for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_base + c * 16, z + c * 16);
       tmem_wait_ld();
 #pragma unroll
-      for (int n = 0; n < 64; ++n) z[n] = fmaxf(z[n] + bias[k * 64 + n], 0.f);
+      for (int n = 0; n < 64; n += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + n);
+        z[n] = fmaxf(z[n] + b4.x, 0.f);
+        z[n + 1] = fmaxf(z[n + 1] + b4.y, 0.f);
+        z[n + 2] = fmaxf(z[n + 2] + b4.z, 0.f);
+        z[n + 3] = fmaxf(z[n + 3] + b4.w, 0.f);
+      }
       if (k + 1 < H) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, jj, z + 8 * jj);
@@ -482,28 +562,89 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(NetDesc net, co
     float y = wout[64];
 #pragma unroll
     for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
-    if (j < q) yout[j] = y;
+    if constexpr (MODE == 0) {
+      if (valid) a.y[j] = y;
+    } else {
+      double e = 0.0;
+      if (valid) {
+        const float v = fmaf(y, md.vrange, md.vmin);
+        a.out[dst] = v;
+        if (MODE == 1 && a.ref) {
+          const double dd = ((double)v - (double)__ldg(a.ref + dst)) / (double)md.vrange;
+          e = dd * dd;
+        }
+      }
+      if (MODE == 1 && a.sse) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (lane == 0 && e != 0.0) atomicAdd(a.sse, e);
+      }
+    }
   }
   mlp_teardown(tmem, lay);
 }
 
-void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
-                             cudaStream_t st) {
+template <int MODE>
+static void launch_forward(const GroupArgs& g, const FwdArgs& a, long long ntiles_hint, cudaStream_t st) {
   Layout L;
-  if (!build_layout(net, L)) return;
-  long long ntiles = (q + kTileM - 1) / kTileM;
-  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles, 148 * L.ctas_per_sm));
-  switch (net.F) {
-#define CASE_F(FF)                                                                                       \
-  case FF:                                                                                               \
-    cudaFuncSetAttribute(forward_tc_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
-    forward_tc_kernel<FF><<<grid, kThreads, L.bytes, st>>>(net, P, x01, q, y, L);                       \
+  if (!build_layout(g.net, L, false)) return;
+  unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles_hint, 148ll * L.ctas_per_sm));
+  switch (g.net.F) {
+#define CASE_F(FF)                                                                                              \
+  case FF:                                                                                                      \
+    cudaFuncSetAttribute(forward_tc_kernel<FF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
+    forward_tc_kernel<FF, MODE><<<grid, kThreads, L.bytes, st>>>(g, a, L);                                     \
     break;
     CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
 #undef CASE_F
     default: break;
   }
   count_launch();
+}
+
+static GroupArgs* single_group(const NetDesc& net, const ModelDev& md) {
+  static thread_local GroupArgs g;
+  g.net = net;
+  g.nmodels = 1;
+  g.md[0] = md;
+  return &g;
+}
+
+void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
+                             cudaStream_t st) {
+  ModelDev md;
+  memset(&md, 0, sizeof md);
+  md.params = const_cast<float*>(P);
+  FwdArgs a;
+  memset(&a, 0, sizeof a);
+  a.x01 = x01;
+  a.y = y;
+  a.q = q;
+  launch_forward<0>(*single_group(net, md), a, (q + kTileM - 1) / kTileM, st);
+}
+
+void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+                           const long long os[3], const float* ref, double* sse, cudaStream_t st) {
+  FwdArgs a;
+  memset(&a, 0, sizeof a);
+  for (int d = 0; d < 3; ++d) { a.res[d] = res[d]; a.os[d] = os[d]; }
+  a.out = out;
+  a.ref = ref;
+  a.sse = sse;
+  long long n = (long long)res[0] * res[1] * res[2];
+  launch_forward<1>(*single_group(net, md), a, (n + kTileM - 1) / kTileM, st);
+}
+
+void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const int* perm,
+                            const int* tile_slot, const int* ntiles_dev, cudaStream_t st) {
+  FwdArgs a;
+  memset(&a, 0, sizeof a);
+  a.xyz = xyz;
+  a.out = out;
+  a.perm = perm;
+  a.tile_slot = tile_slot;
+  a.ntiles_dev = ntiles_dev;
+  launch_forward<2>(g, a, (q + kTileM - 1) / kTileM + g.nmodels, st);
 }
 
 }  // namespace inr

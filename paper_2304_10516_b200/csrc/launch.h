@@ -32,9 +32,11 @@ struct QueryArgs {
   NetDesc net;
   int n[3], N[3], B[3];
   int nblocks;
+  int nmodels;
   ModelDev md[kMaxGroup];
   int16_t slot_of_block[kMaxRouteBlocks];
 };
+inline int qa_nmodels(const QueryArgs& qa) { return qa.nmodels; }
 
 void count_launch(long long n = 1);
 
@@ -71,5 +73,17 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
                    float* dfeat, int Bs, cudaStream_t st);
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
+void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+                           const long long os[3], const float* ref, double* sse, cudaStream_t st);
+void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const int* perm,
+                            const int* tile_slot, const int* ntiles_dev, cudaStream_t st);
+struct QueryBuckets {
+  int* perm;       // [q + 128 nmodels] query index or -1, bucket-sorted, each bucket padded to 128
+  int* tile_slot;  // model slot of each 128-query tile
+  int* ntiles;     // device scalar
+};
+size_t query_workspace_bytes(long long q, int nmodels);
+void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag, void* ws,
+                          QueryBuckets& b, cudaStream_t st);
 
 }  // namespace inr

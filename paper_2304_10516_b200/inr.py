@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libinr.so")
+LIB_PATH = os.environ.get("INR_LIB_PATH") or os.path.join(_HERE, "lib", "libinr.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "inr.h")
 
 if not os.path.exists(LIB_PATH):
@@ -103,6 +103,8 @@ _SIG = {
     "inr_profile_span": (_I32, [ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIG.items():
+    if not hasattr(_lib, _name) and os.environ.get("INR_LIB_PATH"):
+        continue  # an older diagnostic build
     _f = getattr(_lib, _name)
     _f.restype = _res
     _f.argtypes = _args

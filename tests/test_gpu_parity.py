@@ -409,3 +409,50 @@ def test_psnr_target_stopping():
     rep = inr.inr_fit(m, whole_view(vt), 400, 512, go, stream())
     assert rep.reached_target == 1 and rep.probe_psnr >= 45 and rep.steps_taken < 400
     inr.inr_destroy(m)
+
+
+def test_decode_tensor_core_fp16_models():
+    """fp16-MLP models decode on tensor cores: grid (R19 vertex elision) and
+    bucket-sorted queries agree bitwise at the nodes, and both match the oracle
+    within the fp16 tolerance (2e-3 normwise); a point whose block is not in the
+    group decodes to NaN."""
+    blocks = sampler.decompose((48, 48, 48), (16, 16, 16))   # 27 blocks
+    cfg = oracle_config(**CFG1)
+    rng = np.random.default_rng(21)
+    gms, oms = [], {}
+    for b in blocks[:-1]:                                     # the last block is left out
+        p = _perturbed_params(cfg, b, 3, rng)
+        m = make_gpu_model(b, 3, precision=1, **CFG1)
+        inr.inr_set_params(m, p)
+        gms.append(m)
+        oms[b.block_id] = InrModel(cfg, b, 3, params=p)
+    for res in ((16, 16, 16), (32, 32, 32), (13, 5, 21)):
+        out = torch.empty(res[::-1], device="cuda")
+        inr.inr_decode_grid(gms[7], res, out.data_ptr(), None, None, None, stream())
+        torch.cuda.synchronize()
+        assert normwise(out.cpu().numpy(), o_decode.decode_grid(oms[blocks[7].block_id], res)) <= 2e-3
+    full = torch.empty((48, 48, 48), device="cuda")
+    for m, b in zip(gms, blocks):
+        o = b.origin
+        inr.inr_decode_grid(m, (16, 16, 16), full[o[2]:, o[1]:, o[0]:].data_ptr(), (1, 48, 48 * 48), None, None,
+                            stream())
+    z, y, x = np.meshgrid(np.arange(48), np.arange(48), np.arange(48), indexing="ij")
+    pts = np.stack([x.ravel(), y.ravel(), z.ravel()], 1).astype(np.float32)
+    q = torch.empty(pts.shape[0], device="cuda")
+    pd = torch.from_numpy(pts).cuda()
+    inr.inr_decode_group(gms, pd.data_ptr(), pts.shape[0], q.data_ptr(), 0, stream())
+    torch.cuda.synchronize()
+    qn = q.cpu().numpy()
+    last = blocks[-1]
+    own = ((pts[:, 0] >= last.origin[0]) & (pts[:, 1] >= last.origin[1]) & (pts[:, 2] >= last.origin[2]))
+    assert np.all(np.isnan(qn[own])) and not np.any(np.isnan(qn[~own]))
+    assert np.array_equal(qn[~own], full.reshape(-1).cpu().numpy()[~own])
+    rp = synth.random_points(20000, (48, 48, 48))
+    rp = rp[~((rp[:, 0] >= 32) & (rp[:, 1] >= 32) & (rp[:, 2] >= 32))]
+    rd = torch.from_numpy(rp).cuda()
+    rq = torch.empty(rp.shape[0], device="cuda")
+    inr.inr_decode_group(gms, rd.data_ptr(), rp.shape[0], rq.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    assert normwise(rq.cpu().numpy(), o_decode.decode_query(oms, rp)) <= 2e-3
+    for m in gms:
+        inr.inr_destroy(m)

@@ -54,6 +54,7 @@ def gpu_psnrs(precision):
 @pytest.mark.parametrize("precision", [0, 1])
 def test_mean_psnr_within_0p3db(oracle_psnrs, precision):
     g = gpu_psnrs(precision)
+    print("gpu", np.round(g, 2).tolist()); print("oracle", np.round(oracle_psnrs, 2).tolist())
     print(f"precision {precision}: gpu mean {g.mean():.3f} (sd {g.std():.2f}), "
           f"oracle mean {oracle_psnrs.mean():.3f} (sd {oracle_psnrs.std():.2f})")
     assert abs(g.mean() - oracle_psnrs.mean()) <= 0.3
