@@ -300,6 +300,17 @@ def run_ours(args):
     decode = {"voxels_per_s": vox_local * world / (dec_ms / 1e3), "ms": dec_ms, "voxels": vox_local * world,
               "kernel": "decode_grid: " + ("tcgen05 fp16 MLP, R19 vertex elision" if prec else "fp32 CUDA-core MLP"),
               "queries_per_s": nq * world / (q_ms / 1e3), "queries": nq * world, "query_ms": q_ms}
+    if world > 1:   # a18: decoded slabs -> rank 0 (NCCL gather over NVLink), reported separately
+        full = d.gather(out, 0)              # warm (NCCL communicator set-up)
+        del full
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        full = d.gather(out, 0)
+        torch.cuda.synchronize()
+        decode["gather_ms"] = dnr.allreduce_max((time.perf_counter() - t0) * 1e3)
+        decode["gather_bytes"] = int(4 * SIDE ** 3 * world)
+        del full
     done = args.warmup + args.steps + e_steps
     if args.psnr_steps > done:
         d.fit(vol, args.psnr_steps - done, B_U, opts, stream, report=True)

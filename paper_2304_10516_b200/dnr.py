@@ -99,6 +99,35 @@ def allgather_metadata(rows):
     return [r for part in out for r in part]
 
 
+def gather_slabs(local_core, lo, global_dims, dst=0):
+    """Gather every rank's decoded core slab [z][y][x] (origin `lo`, (x, y, z))
+    into the global volume on rank `dst`.
+    Returns the assembled tensor on `dst`, None elsewhere.  Slabs may differ in
+    shape; they are padded to the largest for one dist.gather."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        out = torch.zeros((global_dims[2], global_dims[1], global_dims[0]), dtype=local_core.dtype,
+                          device=local_core.device)
+        z, y, x = local_core.shape
+        out[lo[2]:lo[2] + z, lo[1]:lo[1] + y, lo[0]:lo[0] + x] = local_core
+        return out
+    meta = [None] * dist.get_world_size()
+    dist.all_gather_object(meta, (tuple(lo), tuple(local_core.shape)))
+    n = max(int(torch.tensor(s).prod()) for _, s in meta)
+    buf = torch.zeros(n, dtype=local_core.dtype, device=local_core.device)
+    buf[:local_core.numel()] = local_core.reshape(-1)
+    rank = dist.get_rank()
+    parts = [torch.empty_like(buf) for _ in meta] if rank == dst else None
+    dist.gather(buf, parts, dst=dst)
+    if rank != dst:
+        return None
+    out = torch.zeros((global_dims[2], global_dims[1], global_dims[0]), dtype=local_core.dtype,
+                      device=local_core.device)
+    for (l, shp), p in zip(meta, parts):
+        z, y, x = shp
+        out[l[2]:l[2] + z, l[1]:l[1] + y, l[0]:l[0] + x] = p[:z * y * x].reshape(shp)
+    return out
+
+
 def psnr_from_sse(sse, count):
     """PSNR = -10 log10(MSE), capped at 200 dB (R18)."""
     if count <= 0:
@@ -185,6 +214,17 @@ class DNR:
             refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
             self.inr.inr_decode_grid(m, r, base.data_ptr(), (1, nx, nx * ny), refp,
                                      sse.data_ptr() if sse is not None else None, stream)
+
+    def core_box(self):
+        """(lo, hi inclusive) of this rank's core nodes (the ghost layer excluded)."""
+        hi = [h if h == self.global_dims[d] - 1 else h - 1 for d, h in enumerate(self.hi)]
+        return self.lo, tuple(hi)
+
+    def gather(self, local_out, dst=0):
+        """Gather the decoded local cores (1x decode) to rank `dst` (a18)."""
+        lo, hi = self.core_box()
+        core = local_out[: hi[2] - lo[2] + 1, : hi[1] - lo[1] + 1, : hi[0] - lo[0] + 1].contiguous()
+        return gather_slabs(core, lo, self.global_dims, dst)
 
     def psnr(self, sse_local, count_local):
         sse, cnt = allreduce_sum([sse_local, count_local])

@@ -51,7 +51,14 @@ def _worker(rank, world, port, q):
     sse = dnr.allreduce_sum([0.5 * (rank + 1), 100.0])
     meta = dnr.allgather_metadata([[float(rank), 10.0 + rank]])
     mx = dnr.allreduce_max(3.0 * rank)
-    q.put((rank, rng, sse, meta, mx))
+    import torch
+    # rank r owns z-slab r of a (4, 3, 2r+2)-shaped volume: slabs of different shapes
+    slab = torch.full((2 + rank, 3, 4), float(rank + 1))
+    vol = dnr.gather_slabs(slab, (0, 0, 2 * rank), (4, 3, 5))
+    ok = None
+    if rank == 0:
+        ok = bool((vol[0:2] == 1).all() and (vol[2:5] == 2).all())
+    q.put((rank, rng, sse, meta, mx, ok))
     dist.destroy_process_group()
 
 
@@ -65,7 +72,8 @@ def test_collectives_world2_gloo():
     res = sorted(q.get(timeout=120) for _ in range(2))
     for p in ps:
         p.join(60)
-    for rank, rng, sse, meta, mx in res:
+    assert res[0][5] is True and res[1][5] is None     # slab gather to rank 0 (a18)
+    for rank, rng, sse, meta, mx, _ in res:
         assert rng == (-2.0, 1.0)                         # S:L275-277 example
         assert sse == [1.5, 200.0]
         assert meta == [[0.0, 10.0], [1.0, 11.0]]
