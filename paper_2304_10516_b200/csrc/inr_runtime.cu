@@ -59,10 +59,10 @@ static inr_status cuda_fail(cudaError_t e, const char* what) {
 extern "C" const char* inr_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ profiling
-enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_SAMPLE, PK_ENCODE_FWD, PK_MLP_TC, PK_ENCODE_BWD, PK_ADAM,
+enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_SAMPLE, PK_ENCODE_FWD, PK_PREP, PK_MLP_TC, PK_ENCODE_BWD, PK_ADAM,
                 PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE, PK_COUNT };
-static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "sample", "encode_fwd", "mlp_tc", "encode_bwd",
-                                           "adam", "decode_grid", "decode_query", "probe", "range"};
+static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "sample", "encode_fwd", "prep_image", "mlp_tc",
+                                           "encode_bwd", "adam", "decode_grid", "decode_query", "probe", "range"};
 struct ProfRec { int kind; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_event_pool;
@@ -521,17 +521,19 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   auto enqueue_step = [&](cudaStream_t s) {
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
-      { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, s); }
       if (tc) {
+        { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, 0, s); }
         { ProfScope p(PK_SAMPLE, s); launch_sample(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
-        { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.feat, ws.samples, ws.dfeat, ws.Bs, s); }
+        { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
+        { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.dfeat, ws.Bs, s); }
         { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, ws, s); }
+        { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
       } else {
-        ProfScope p(PK_FIT_FP32, s);
-        launch_fit_simt(g, g.nmodels, fs, s);
+        { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, 0, s); }
+        { ProfScope p(PK_FIT_FP32, s); launch_fit_simt(g, g.nmodels, fs, s); }
+        { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
       }
-      { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
     }
   };
   struct WsFree {
@@ -539,7 +541,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     ~WsFree() { if (p) cudaFreeAsync(p, s); }
   } ws_free{ws_mem, st};
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = (tc ? 6 : 3) * nchunks;
+  const int launches_per_step = (tc ? 7 : 3) * nchunks;
   // CUDA graphs (launch-gap free): without probing, capture one step and replay it
   // per step; while profiling, capture the whole loop (with its event records)
   // once, so per-kernel timings come from the same graph execution.

@@ -35,40 +35,50 @@ __global__ void __launch_bounds__(kLmThreads) sample_kernel(GroupArgs g, FitScal
   samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], sample_target(md, x));
 }
 
+// Writes straight into the tensor-core MLP's h_0 tile images (canonical layout,
+// see tc_common.cuh): sample i -> tile i/128, row i%128, columns [l F, l F + F).
+// Padding samples (total <= i < Bs) write zeros; level 0 also writes the
+// constant-ones group (column LF).
 template <int F>
 __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, FitScalars fs,
                                                                  const float4* __restrict__ samples,
-                                                                 __half* __restrict__ feat, int Bs) {
+                                                                 uint8_t* __restrict__ featimg, int Bs,
+                                                                 FeatGeom geom) {
   const int m = blockIdx.z, l = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
   const int i = blockIdx.x * kLmThreads + threadIdx.x;
-  if (i >= total) return;
-  const float4 s = __ldg(samples + (size_t)m * Bs + i);
-  const float x[3] = {s.x, s.y, s.z};
+  if (i >= Bs) return;
   float f[F];
-  encode_level<F>(md.params, g.net.lv[l], g.net.table_mask, x, f);
-  __half* o = feat + (((size_t)m * g.net.L + l) * Bs + i) * F;
+#pragma unroll
+  for (int j = 0; j < F; ++j) f[j] = 0.f;
+  if (i < total) {
+    const float4 s = __ldg(samples + (size_t)m * Bs + i);
+    const float x[3] = {s.x, s.y, s.z};
+    encode_level<F>(md.params, g.net.lv[l], g.net.table_mask, x, f);
+  }
+  const int r = i & 127;
+  uint8_t* tile = featimg + ((size_t)m * (Bs >> 7) + (i >> 7)) * geom.tile_bytes;
+  uint8_t* row = tile + (r & 7) * 16 + (r >> 3) * geom.sbo;
+  const int c = l * F;
   if constexpr (F == 1) {
-    o[0] = __float2half_rn(f[0]);
+    *reinterpret_cast<__half*>(row + (c >> 3) * 128 + (c & 7) * 2) = __float2half_rn(f[0]);
   } else {
 #pragma unroll
-    for (int j = 0; j < F; j += 2) *reinterpret_cast<__half2*>(o + j) = __floats2half2_rn(f[j], f[j + 1]);
+    for (int j = 0; j < F; j += 2)
+      *reinterpret_cast<__half2*>(row + ((c + j) >> 3) * 128 + ((c + j) & 7) * 2) = __floats2half2_rn(f[j], f[j + 1]);
   }
+  if (l == 0 && geom.ones)
+    *reinterpret_cast<uint4*>(row + (g.net.LF >> 3) * 128) = make_uint4(0x3C00u, 0u, 0u, 0u);
 }
 
+// Scatter-add of samples [i0, i1) of model m at level l.  Small dense
+// levels accumulate in shared memory first and flush once.
 template <int F>
-__global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, FitScalars fs,
-                                                                 const float4* __restrict__ samples,
-                                                                 const float* __restrict__ dfeat, int Bs) {
-  extern __shared__ __align__(16) unsigned char acc_raw[];
-  const int m = blockIdx.z, l = blockIdx.y;
-  const ModelDev& md = g.md[m];
+__device__ __forceinline__ void scatter_chunk(const GroupArgs& g, const ModelDev& md, int m, int l,
+                                              const float4* __restrict__ samples, const float* __restrict__ dfeat,
+                                              int Bs, int i0, int i1, unsigned char* acc_raw) {
   const LevelInfo& lv = g.net.lv[l];
-  const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
-  const int i0 = blockIdx.x * kBwdChunk;
-  if (i0 >= total) return;
-  const int i1 = min(i0 + kBwdChunk, total);
   const int nfl = (int)lv.size * F;
   const bool small = nfl <= kSmemAccFloats;
   float* G = md.grads;
@@ -76,13 +86,13 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
   float* accf = reinterpret_cast<float*>(acc_raw);
   unsigned long long* accx = reinterpret_cast<unsigned long long*>(acc_raw);
   if (small) {
-    for (int e = threadIdx.x; e < nfl; e += kLmThreads) {
+    for (int e = threadIdx.x; e < nfl; e += blockDim.x) {
       if (GX) accx[e] = 0ull; else accf[e] = 0.f;
     }
     __syncthreads();
   }
   const float* dfl = dfeat + ((size_t)m * g.net.L + l) * Bs * F;
-  for (int i = i0 + threadIdx.x; i < i1; i += kLmThreads) {
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const float4 s = __ldg(samples + (size_t)m * Bs + i);
     const float x[3] = {s.x, s.y, s.z};
     float d[F];
@@ -117,7 +127,7 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
   }
   if (small) {
     __syncthreads();
-    for (int e = threadIdx.x; e < nfl; e += kLmThreads) {
+    for (int e = threadIdx.x; e < nfl; e += blockDim.x) {
       if (GX) {
         unsigned long long v = accx[e];
         if (v) atomicAdd(GX + lv.offset + e, v);
@@ -126,7 +136,21 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
         if (v != 0.f) atomicAdd(G + lv.offset + e, v);
       }
     }
+    __syncthreads();
   }
+}
+
+template <int F>
+__global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, FitScalars fs,
+                                                                 const float4* __restrict__ samples,
+                                                                 const float* __restrict__ dfeat, int Bs) {
+  extern __shared__ __align__(16) unsigned char acc_raw[];
+  const int m = blockIdx.z, l = blockIdx.y;
+  const ModelDev& md = g.md[m];
+  const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
+  const int i0 = blockIdx.x * kBwdChunk;
+  if (i0 >= total) return;
+  scatter_chunk<F>(g, md, m, l, samples, dfeat, Bs, i0, min(i0 + kBwdChunk, total), acc_raw);
 }
 
 // ------------------------------------------------------- query bucketing
@@ -216,20 +240,27 @@ void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, fl
   }
 
 size_t lm_workspace_bytes(const NetDesc& net, int nmodels, int Bs) {
+  FeatGeom geom;
+  uint32_t img = 0;
+  tc_fit_geometry(net, &geom, &img);
   size_t s = (size_t)nmodels * Bs;
-  return s * sizeof(float4) + s * net.LF * sizeof(__half) + s * net.LF * sizeof(float) + 3 * 256;
+  return s * sizeof(float4) + (size_t)nmodels * (Bs / 128) * geom.tile_bytes + s * net.LF * sizeof(float) +
+         (size_t)nmodels * img + 4 * 256;
 }
 
 LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs) {
   LmWorkspace w;
+  tc_fit_geometry(net, &w.geom, &w.img_bytes);
   size_t s = (size_t)nmodels * Bs;
   char* p = (char*)base;
   auto align = [](size_t v) { return (v + 255) / 256 * 256; };
   w.samples = reinterpret_cast<float4*>(p);
   p += align(s * sizeof(float4));
-  w.feat = reinterpret_cast<__half*>(p);
-  p += align(s * net.LF * sizeof(__half));
+  w.featimg = reinterpret_cast<uint8_t*>(p);
+  p += align((size_t)nmodels * (Bs / 128) * w.geom.tile_bytes);
   w.dfeat = reinterpret_cast<float*>(p);
+  p += align(s * net.LF * sizeof(float));
+  w.wimg = reinterpret_cast<uint8_t*>(p);
   w.Bs = Bs;
   return w;
 }
@@ -242,8 +273,9 @@ void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
 
 void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w,
                        cudaStream_t st) {
-  dim3 grid((fs.B_u + fs.B_b + kLmThreads - 1) / kLmThreads, g.net.L, nmodels);
-  LM_DISPATCH_F(g.net.F, encode_fwd_kernel<FF><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.feat, w.Bs));
+  dim3 grid((w.Bs + kLmThreads - 1) / kLmThreads, g.net.L, nmodels);
+  LM_DISPATCH_F(g.net.F,
+                encode_fwd_kernel<FF><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.featimg, w.Bs, w.geom));
   count_launch();
 }
 

@@ -8,6 +8,7 @@
 // encode and scatter code of common.cuh.
 #include <algorithm>
 
+#include "adam.cuh"
 #include "common.cuh"
 #include "launch.h"
 
@@ -42,7 +43,7 @@ __global__ void init_params_kernel(NetDesc net, float* __restrict__ params, uint
 
 // --------------------------------------------------------- step bookkeeping
 // Zero this step's gradient accumulators and loss sums; step_cur <- step_total++.
-__global__ void step_begin_kernel(GroupArgs g) {
+__global__ void step_begin_kernel(GroupArgs g, long long zero_from) {
   const ModelDev& md = g.md[blockIdx.y];
   long long n = g.net.nparams;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -55,11 +56,10 @@ __global__ void step_begin_kernel(GroupArgs g) {
   long long stride = (long long)gridDim.x * blockDim.x;
   long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (md.grads_fx) {
-    for (long long i = i0; i < n; i += stride) md.grads_fx[i] = 0ull;
-  } else {
+    for (long long i = zero_from + i0; i < n; i += stride) md.grads_fx[i] = 0ull;
+  } else {   // zero_from and n are multiples of 64
     float4* g4 = reinterpret_cast<float4*>(md.grads);
-    for (long long i = i0; i < n / 4; i += stride) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (long long i = (n / 4) * 4 + i0; i < n; i += stride) md.grads[i] = 0.f;
+    for (long long i = zero_from / 4 + i0; i < n / 4; i += stride) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -256,57 +256,9 @@ __global__ void __launch_bounds__(kTile) fit_simt_kernel(GroupArgs g, FitScalars
 // Deterministic mode converts the exact int64 sums to fp32 first.
 __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
   const ModelDev& md = g.md[blockIdx.y];
-  const long long n = g.net.nparams;
-  const long long s = *md.step_cur;
-  const double lr = as.lr0 * pow(as.lr_decay, (double)(s / as.lr_step));
-  const double bc1 = 1.0 - pow(as.beta1, (double)(s + 1));
-  const double bc2 = 1.0 - pow(as.beta2, (double)(s + 1));
-  const float step_size = (float)(lr / bc1);
-  const float inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
-  const float b1 = as.b1, b2 = as.b2, eps = as.eps;
-  const float ob1 = as.ob1, ob2 = as.ob2;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  bool bad = false;
-  float* __restrict__ P = md.params;
-  float* __restrict__ G = md.grads;
-  float* __restrict__ M = md.adam_m;
-  float* __restrict__ V = md.adam_v;
-  if (md.grads_fx) {
-    const float sc = 1.f / (float)(1ll << kFixedShift);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-      float gi = (float)((double)(long long)md.grads_fx[i] * (double)sc);
-      G[i] = gi;
-      float m = fmaf(b1, M[i], ob1 * gi), v = fmaf(b2, V[i], ob2 * gi * gi);
-      float p = P[i] - step_size * m / (sqrtf(v) * inv_sqrt_bc2 + eps);
-      M[i] = m; V[i] = v; P[i] = p;
-      bad |= !isfinite(p);
-    }
-  } else {
-    const long long n4 = n / 4;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
-      float4 gg = reinterpret_cast<const float4*>(G)[i];
-      float4 mm = reinterpret_cast<float4*>(M)[i];
-      float4 vv = reinterpret_cast<float4*>(V)[i];
-      float4 pp = reinterpret_cast<float4*>(P)[i];
-#define ADAM1(c)                                                              \
-  mm.c = fmaf(b1, mm.c, ob1 * gg.c);                                          \
-  vv.c = fmaf(b2, vv.c, ob2 * gg.c * gg.c);                                   \
-  pp.c = pp.c - step_size * mm.c / (sqrtf(vv.c) * inv_sqrt_bc2 + eps);        \
-  bad |= !isfinite(pp.c);
-      ADAM1(x) ADAM1(y) ADAM1(z) ADAM1(w)
-#undef ADAM1
-      reinterpret_cast<float4*>(M)[i] = mm;
-      reinterpret_cast<float4*>(V)[i] = vv;
-      reinterpret_cast<float4*>(P)[i] = pp;
-    }
-    for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-      float gi = G[i];
-      float m = fmaf(b1, M[i], ob1 * gi), v = fmaf(b2, V[i], ob2 * gi * gi);
-      float p = P[i] - step_size * m / (sqrtf(v) * inv_sqrt_bc2 + eps);
-      M[i] = m; V[i] = v; P[i] = p;
-      bad |= !isfinite(p);
-    }
-  }
+  const AdamStep a = adam_step_scalars(*md.step_cur, as.lr0, as.lr_decay, as.lr_step, as.beta1, as.beta2, as.b1,
+                                       as.b2, as.ob1, as.ob2, as.eps);
+  const bool bad = adam_range(md, a, 0, g.net.nparams, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(md.flag, 1);
 }
 
@@ -495,9 +447,9 @@ void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t
   count_launch();
 }
 
-void launch_step_begin(const GroupArgs& g, int nmodels, cudaStream_t st) {
-  int bx = (int)std::min<long long>((g.net.nparams / 4 + 255) / 256, 148 * 4 / max(1, nmodels) + 1);
-  step_begin_kernel<<<dim3(max(bx, 1), nmodels), 256, 0, st>>>(g);
+void launch_step_begin(const GroupArgs& g, int nmodels, long long zero_from, cudaStream_t st) {
+  int bx = (int)std::min<long long>(((g.net.nparams - zero_from) / 4 + 255) / 256, 148 * 4 / max(1, nmodels) + 1);
+  step_begin_kernel<<<dim3(max(bx, 1), nmodels), 256, 0, st>>>(g, zero_from);
   count_launch();
 }
 

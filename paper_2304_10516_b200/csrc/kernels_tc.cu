@@ -73,6 +73,66 @@ __device__ __forceinline__ uint32_t mlp_setup(const NetDesc& net, const float* _
   return *tslot;
 }
 
+// Fit-kernel setup: TMEM allocation, barriers, the constant ones groups of
+// h_1..h_{H-1}, and one TMA bulk copy of the step's prepared weight image.
+__device__ __forceinline__ uint32_t mlp_setup_fit(const NetDesc& net, const uint8_t* wimg, uint8_t* smem,
+                                                  const Layout& lay) {
+  const int t = threadIdx.x, warp = t >> 5;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(lay.ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (t == 0) {
+    mbar_init(smem_u32(smem + lay.mbar), 1);
+    mbar_init(smem_u32(smem + lay.mbar_img), 1);
+    mbar_init(smem_u32(smem + lay.mbar_feat[0]), 1);
+    mbar_init(smem_u32(smem + lay.mbar_feat[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (lay.ones && t < kTileM) {
+    for (int k = 1; k < net.H; ++k) {
+      uint4 u = make_uint4(0x3C00u, 0u, 0u, 0u);   // half(1.0), then zeros
+      *reinterpret_cast<uint4*>(smem + lay.h[k] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[k] +
+                                (net.in_dim[k] >> 3) * 128) = u;
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    mbar_expect_tx(smem_u32(smem + lay.mbar_img), lay.img_bytes);
+    bulk_g2s(smem_u32(smem), wimg, lay.img_bytes, smem_u32(smem + lay.mbar_img));
+  }
+  fence_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  mbar_wait(smem_u32(smem + lay.mbar_img), 0);
+  return *tslot;
+}
+
+// Per step: each model's fp32 MLP weights -> the fp16 weight image (canonical
+// tiles + fp32 biases and output layer) that every fit CTA bulk-copies.
+__global__ void __launch_bounds__(256) prep_image_kernel(GroupArgs g, Layout lay, uint8_t* __restrict__ wimg) {
+  const NetDesc& net = g.net;
+  const float* __restrict__ P = g.md[blockIdx.x].params;
+  uint8_t* dst = wimg + (size_t)blockIdx.x * lay.img_bytes;
+  for (int k = 0; k < net.H; ++k) {
+    const int in = net.in_dim[k];
+    for (int n = threadIdx.y; n < 64; n += blockDim.y) {
+      for (int i = threadIdx.x; i < in; i += blockDim.x)
+        *reinterpret_cast<__half*>(dst + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) =
+            __float2half_rn(P[net.w_off[k] + n * in + i]);
+    }
+  }
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  float* bias = reinterpret_cast<float*>(dst + lay.bias);
+  float* wout = reinterpret_cast<float*>(dst + lay.wout);
+  for (int e = t; e < net.H * 64; e += 256) bias[e] = net.bias ? P[net.b_off[e / 64] + (e % 64)] : 0.f;
+  for (int i = t; i < 64; i += 256) wout[i] = P[net.w_off[net.H] + i];
+  if (t == 0) wout[64] = net.bias ? P[net.b_off[net.H]] : 0.f;
+}
+
 __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
   fence_before();
   __syncthreads();
@@ -88,7 +148,8 @@ __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
 // [model][level][Bs][F]; adds dW, db into the model's gradient.
 template <int F>
 __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitScalars fs, Layout lay,
-                                                             float loss_scale, const __half* __restrict__ feat,
+                                                             float loss_scale, const uint8_t* __restrict__ featimg,
+                                                             const uint8_t* __restrict__ wimg,
                                                              const float4* __restrict__ samples,
                                                              float* __restrict__ dfeat, int Bs) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -103,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
   float* __restrict__ G = md.grads;
   unsigned long long* __restrict__ GX = md.grads_fx;
   const float inv_scale = 1.f / loss_scale;
-  const __half* featm = feat + (size_t)m * L * Bs * F;
+  const uint8_t* featm = featimg + (size_t)m * (Bs / kTileM) * lay.feat_tile_bytes;
   float* dfeatm = dfeat + (size_t)m * L * Bs * F;
 
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
@@ -111,48 +172,32 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
   float* red = reinterpret_cast<float*>(smem + lay.red);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
   for (int i = t; i < 66; i += kThreads) red[i] = 0.f;
-  const uint32_t tmem = mlp_setup(net, md.params, smem, lay, true);
+  const uint32_t tmem = mlp_setup_fit(net, wimg + (size_t)m * lay.img_bytes, smem, lay);
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0;
   bool first = true;
   const float lam = B_b > 0 ? fs.lambda : 0.f;
+  const uint32_t hbuf[2] = {smem_u32(smem + lay.h[0]), smem_u32(smem + lay.h0b)};
+  const uint32_t fbar[2] = {smem_u32(smem + lay.mbar_feat[0]), smem_u32(smem + lay.mbar_feat[1])};
+  if (t == 0 && (int)blockIdx.x < ntiles) {   // prefetch the first feature tile
+    mbar_expect_tx(fbar[0], lay.feat_tile_bytes);
+    bulk_g2s(hbuf[0], featm + (size_t)blockIdx.x * lay.feat_tile_bytes, lay.feat_tile_bytes, fbar[0]);
+  }
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int i = tile * kTileM + t;
     const bool valid = i < total;
     const bool is_b = i >= fs.B_u;
     const float target = valid ? samples[(size_t)m * Bs + i].w : 0.f;
-    // ---- level-major fp16 features -> canonical h_0 row (16 B = 8 columns per chunk)
-    for (int j = 0; j * 8 < net.LF; ++j) {
-      uint4 u = make_uint4(0u, 0u, 0u, 0u);
-      if (valid) {
-        if constexpr (F == 1) {
-          uint32_t w[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const unsigned short* p = reinterpret_cast<const unsigned short*>(featm);
-            uint32_t lo = p[(size_t)(8 * j + 2 * q) * Bs + i], hi = p[(size_t)(8 * j + 2 * q + 1) * Bs + i];
-            w[q] = lo | (hi << 16);
-          }
-          u = make_uint4(w[0], w[1], w[2], w[3]);
-        } else if constexpr (F == 2) {
-          const uint32_t* p = reinterpret_cast<const uint32_t*>(featm);
-          u = make_uint4(p[(size_t)(4 * j) * Bs + i], p[(size_t)(4 * j + 1) * Bs + i], p[(size_t)(4 * j + 2) * Bs + i],
-                         p[(size_t)(4 * j + 3) * Bs + i]);
-        } else if constexpr (F == 4) {
-          const uint2* p = reinterpret_cast<const uint2*>(featm);
-          uint2 a = p[(size_t)(2 * j) * Bs + i], b = p[(size_t)(2 * j + 1) * Bs + i];
-          u = make_uint4(a.x, a.y, b.x, b.y);
-        } else {
-          u = reinterpret_cast<const uint4*>(featm)[(size_t)j * Bs + i];
-        }
-      }
-      *reinterpret_cast<uint4*>(smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0] + j * 128) = u;
+    const int b = it & 1;
+    const uint32_t h0 = hbuf[b];
+    if (t == 0 && tile + (int)gridDim.x < ntiles) {   // prefetch the next tile into the other buffer
+      mbar_expect_tx(fbar[b ^ 1], lay.feat_tile_bytes);
+      bulk_g2s(hbuf[b ^ 1], featm + (size_t)(tile + gridDim.x) * lay.feat_tile_bytes, lay.feat_tile_bytes,
+               fbar[b ^ 1]);
     }
-    fence_async_smem();
-    fence_before();
-    __syncthreads();
-
+    mbar_wait(fbar[b], (uint32_t)(it >> 1) & 1u);
     // ---- forward through the hidden layers
     uint32_t mask[kMaxLayers][2];
     float hH[64];
@@ -160,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
       const int in = net.in_dim[k];
       if (t == 0) {
         fence_after();
-        gemm(tmem, smem_u32(smem + lay.h[k]), 128, lay.h_sbo[k], 256, smem_u32(smem + lay.w[k]), 128,
+        gemm(tmem, k == 0 ? h0 : smem_u32(smem + lay.h[k]), 128, lay.h_sbo[k], 256, smem_u32(smem + lay.w[k]), 128,
              lay.w_sbo[k], 256, in / 16, make_idesc(128, 64, 0, 0), false);
         mma_commit(mbar);
       }
@@ -173,8 +218,13 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
       tmem_wait_ld();
       uint32_t m0 = 0, m1 = 0;
 #pragma unroll
+      for (int n = 0; n < 64; n += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + n);
+        z[n] += b4.x; z[n + 1] += b4.y; z[n + 2] += b4.z; z[n + 3] += b4.w;
+      }
+#pragma unroll
       for (int n = 0; n < 64; ++n) {
-        float v = z[n] + bias[k * 64 + n];
+        float v = z[n];
         bool pos = v > 0.f && valid;
         if (n < 32) m0 |= (uint32_t)pos << n; else m1 |= (uint32_t)pos << (n - 32);
         z[n] = pos ? v : 0.f;
@@ -250,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
         fence_after();
         // dW_k (+ db_k in column in_k): A = dz^T (MN-major), B = h_k (MN-major), K = 128 samples
         gemm(tmem + lay.col_dw[k], smem_u32(smem + lay.dz), lay.dz_sbo, 128, 2 * lay.dz_sbo,
-             smem_u32(smem + lay.h[k]), lay.h_sbo[k], 128, 2 * lay.h_sbo[k], kTileM / 16,
+             k == 0 ? h0 : smem_u32(smem + lay.h[k]), lay.h_sbo[k], 128, 2 * lay.h_sbo[k], kTileM / 16,
              make_idesc(64, in + ones, 1, 1), !first);
         // dh_k = dz_k W_k: A = dz (K-major, K = 64 outputs), B = W_k (MN-major, N = in_k)
         gemm(tmem, smem_u32(smem + lay.dz), 128, lay.dz_sbo, 256, smem_u32(smem + lay.w[k]), lay.w_sbo[k], 128,
@@ -343,19 +393,29 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
     off += bytes;
     return o;
   };
+  // the weight image (copied as one block in the fit kernel): weight tiles, biases, output layer
+  for (int k = 0; k < net.H; ++k) {
+    L.w_sbo[k] = (uint32_t)(net.in_dim[k] / 8) * 128;
+    L.w[k] = take(64 * net.in_dim[k] * 2, 1024);
+  }
+  L.bias = take(net.H * 64 * 4, 16);
+  L.wout = take(68 * 4, 16);
+  L.img_bytes = (off + 15) / 16 * 16;
+  off = L.img_bytes;
   for (int k = 0; k < net.H; ++k) {
     int in = net.in_dim[k];
-    L.w_sbo[k] = (uint32_t)(in / 8) * 128;
-    L.w[k] = take(64 * in * 2, 1024);
     L.h_sbo[k] = (uint32_t)((in + L.ones) / 8) * 128;
     L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
   }
+  L.feat_tile_bytes = kTileM * (net.LF + L.ones) * 2;
+  if (train) L.h0b = take(L.feat_tile_bytes, 1024);
   L.dz_sbo = 8 * 128;
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
-  L.bias = take(net.H * 64 * 4, 16);
-  L.wout = take(65 * 4, 16);
   L.red = take(66 * 4, 16);
   L.mbar = take(8, 8);
+  L.mbar_img = take(8, 8);
+  L.mbar_feat[0] = take(8, 8);
+  L.mbar_feat[1] = take(8, 8);
   L.tslot = take(4, 4);
   // TMEM: [0, 64) layer accumulator; then dW_k (M = 64 rows, in_k + ones columns)
   // (8-column granularity; the last region is padded so 16-column loads stay inside)
@@ -392,8 +452,23 @@ static float loss_scale_for(int B_u) {
   return (float)(1 << e);
 }
 
-void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const __half* feat, const float4* samples,
-                   float* dfeat, int Bs, cudaStream_t st) {
+bool tc_fit_geometry(const NetDesc& net, FeatGeom* geom, uint32_t* img_bytes) {
+  Layout L;
+  if (!build_layout(net, L)) return false;
+  if (geom) { geom->sbo = L.h_sbo[0]; geom->tile_bytes = L.feat_tile_bytes; geom->ones = L.ones; }
+  if (img_bytes) *img_bytes = L.img_bytes;
+  return true;
+}
+
+void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStream_t st) {
+  Layout L;
+  if (!build_layout(g.net, L)) return;
+  prep_image_kernel<<<nmodels, dim3(64, 4), 0, st>>>(g, L, wimg);
+  count_launch();
+}
+
+void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
+                   const float4* samples, float* dfeat, int Bs, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L)) return;
   const int total = fs.B_u + fs.B_b;
@@ -406,7 +481,7 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
 #define CASE_F(FF)                                                                                   \
   case FF:                                                                                           \
     cudaFuncSetAttribute(mlp_fit_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
-    mlp_fit_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls, feat, samples, dfeat, Bs);     \
+    mlp_fit_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls, featimg, wimg, samples, dfeat, Bs); \
     break;
     CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
 #undef CASE_F

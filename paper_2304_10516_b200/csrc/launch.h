@@ -42,7 +42,7 @@ void count_launch(long long n = 1);
 
 void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t k1, uint32_t block_id,
                         cudaStream_t st);
-void launch_step_begin(const GroupArgs& g, int nmodels, cudaStream_t st);
+void launch_step_begin(const GroupArgs& g, int nmodels, long long zero_from, cudaStream_t st);
 void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
 void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st);
 void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st);
@@ -57,20 +57,34 @@ void launch_debug_forward_simt(const NetDesc& net, const float* P, const float* 
                                cudaStream_t st);
 
 // level-major fp16 fit pipeline — kernels_lm.cu (CUDA cores) + kernels_tc.cu (tcgen05)
+// Geometry of the fp16 feature tile images the encode writes and the tensor-core
+// MLP bulk-copies: 128 samples x (LF + ones) columns in the canonical layout.
+struct FeatGeom {
+  uint32_t sbo;         // row-group stride (bytes)
+  uint32_t tile_bytes;  // bytes per 128-sample tile
+  int ones;             // width of the constant-ones column group (0 or 8)
+};
+bool tc_fit_geometry(const NetDesc& net, FeatGeom* geom, uint32_t* img_bytes);
+
 struct LmWorkspace {
   float4* samples;   // [model][Bs] (x, y, z, target)
-  __half* feat;      // [model][level][Bs][F] fp16
+  uint8_t* featimg;  // [model][Bs/128] fp16 h_0 tile images
   float* dfeat;      // [model][level][Bs][F] fp32
-  int Bs;            // per-model sample stride
+  uint8_t* wimg;     // [model] fp16 weight images (tiles, biases, output layer)
+  FeatGeom geom;
+  uint32_t img_bytes;
+  int Bs;            // per-model sample stride (multiple of 128)
 };
 size_t lm_workspace_bytes(const NetDesc& net, int nmodels, int Bs);
 LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs);
+void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStream_t st);
+
 void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 void launch_encode_bwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 bool tc_supported(const NetDesc& net);
-void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const __half* feat, const float4* samples,
-                   float* dfeat, int Bs, cudaStream_t st);
+void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
+                   const float4* samples, float* dfeat, int Bs, cudaStream_t st);
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
 void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,

@@ -25,7 +25,12 @@ struct Layout {
   uint32_t bias;                 // fp32 [H][64]
   uint32_t wout;                 // fp32 W_H[64], then b_H
   uint32_t red;                  // fp32 dW_H[64], db_H, pad
-  uint32_t mbar;                 // 8 B
+  uint32_t mbar;                 // 8 B: MMA completion
+  uint32_t mbar_img;             // 8 B: weight-image bulk copy (fit)
+  uint32_t mbar_feat[2];         // 8 B each: feature-tile bulk copies (fit, double buffered)
+  uint32_t h0b;                  // second h_0 buffer (fit)
+  uint32_t img_bytes;            // [0, img_bytes): weight tiles + biases + output layer (the weight image)
+  uint32_t feat_tile_bytes;      // one 128-sample h_0 tile image
   uint32_t tslot;                // 4 B: TMEM base address
   uint32_t bytes;                // dynamic smem requested
   uint32_t col_dw[kMaxLayers];   // TMEM column of the dW_k accumulator
@@ -85,6 +90,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// TMA bulk copy global -> shared, completion (bytes) reported on an mbarrier.
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   dst_smem),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // 16 consecutive fp32 columns of this thread's TMEM lane.
