@@ -522,7 +522,8 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
       if (tc) {
-        { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, 0, s); }
+        // (the gradient is zeroed inside encode_fwd; step_begin only advances the step)
+        { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, m0->net.nparams, s); }
         { ProfScope p(PK_SAMPLE, s); launch_sample(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }

@@ -47,6 +47,21 @@ __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, Fit
   const int m = blockIdx.z, l = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
+  {
+    // this step's gradient zeroing rides along (this kernel is L1-gather bound):
+    // CTA (x, l) of model m clears one contiguous slice of the model's gradient
+    const long long n4 = g.net.nparams / 4;   // nparams is a multiple of 64
+    const long long ctas = (long long)gridDim.x * gridDim.y;
+    const long long per = (n4 + ctas - 1) / ctas;
+    const long long c = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+    const long long a = c * per, b = min(a + per, n4);
+    if (md.grads_fx) {
+      for (long long q = 4 * a + threadIdx.x; q < 4 * b; q += blockDim.x) md.grads_fx[q] = 0ull;
+    } else {
+      float4* g4 = reinterpret_cast<float4*>(md.grads);
+      for (long long q = a + threadIdx.x; q < b; q += blockDim.x) g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
   const int i = blockIdx.x * kLmThreads + threadIdx.x;
   if (i >= Bs) return;
   float f[F];

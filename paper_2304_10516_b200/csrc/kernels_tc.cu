@@ -117,14 +117,16 @@ __global__ void __launch_bounds__(256) prep_image_kernel(GroupArgs g, Layout lay
   const NetDesc& net = g.net;
   const float* __restrict__ P = g.md[blockIdx.x].params;
   uint8_t* dst = wimg + (size_t)blockIdx.x * lay.img_bytes;
+  // CTA (model, y) converts rows y, y + gridDim.y, ... of every weight tile
   for (int k = 0; k < net.H; ++k) {
     const int in = net.in_dim[k];
-    for (int n = threadIdx.y; n < 64; n += blockDim.y) {
+    for (int n = blockIdx.y * blockDim.y + threadIdx.y; n < 64; n += gridDim.y * blockDim.y) {
       for (int i = threadIdx.x; i < in; i += blockDim.x)
         *reinterpret_cast<__half*>(dst + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) =
             __float2half_rn(P[net.w_off[k] + n * in + i]);
     }
   }
+  if (blockIdx.y != 0) return;
   const int t = threadIdx.y * blockDim.x + threadIdx.x;
   float* bias = reinterpret_cast<float*>(dst + lay.bias);
   float* wout = reinterpret_cast<float*>(dst + lay.wout);
@@ -463,7 +465,7 @@ bool tc_fit_geometry(const NetDesc& net, FeatGeom* geom, uint32_t* img_bytes) {
 void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L)) return;
-  prep_image_kernel<<<nmodels, dim3(64, 4), 0, st>>>(g, L, wimg);
+  prep_image_kernel<<<dim3(nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg);
   count_launch();
 }
 
