@@ -189,8 +189,10 @@ __global__ void route_kernel(QueryArgs qa, const float* __restrict__ xyz, long l
   const int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
   const int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
   slot_of[j] = slot;
-  if (slot >= 0) atomicAdd(counts + slot, 1);
-  else out[j] = __int_as_float(0x7fc00000);
+  // warp-aggregated count: one atomic per distinct block in the warp
+  const unsigned peers = __match_any_sync(__activemask(), slot);
+  if (slot >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + slot, __popc(peers));
+  if (slot < 0) out[j] = __int_as_float(0x7fc00000);
   if (outside && dflag) atomicOr(dflag, 1);
 }
 
@@ -214,8 +216,13 @@ __global__ void bucket_scatter_kernel(const int* __restrict__ slot_of, long long
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= q) return;
   const int s = slot_of[j];
+  const unsigned peers = __match_any_sync(__activemask(), s);
   if (s < 0) return;
-  perm[offsets[s] + atomicAdd(cursor + s, 1)] = (int)j;
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(cursor + s, __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  perm[offsets[s] + base + __popc(peers & ((1u << lane) - 1u))] = (int)j;
 }
 
 size_t query_workspace_bytes(long long q, int nmodels) {
