@@ -1,0 +1,291 @@
+"""configs.py — runs BASELINE.json's five configurations through the library
+and records fit coords/s, decode voxels/s (or queries/s) and PSNR @ compression
+ratio for each.  The headline bench line is bench.py (cfg2);
+this script is the per-config evidence, written to profiles/.
+
+  python configs.py [--only cfg1,cfg3] [--out profiles/r1_configs.json] [--world-slice]
+
+Every config runs on ONE GPU: cfg3 fits all 64 blocks on it, cfg5 fits one
+GPU's share (64 of the 512 blocks: a 1024 x 1024 x 128 slab of the 1024^3
+volume).  Times are CUDA events on the launching stream.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2304_10516_b200 import dnr, inr  # noqa: E402
+
+NET2 = dict(levels=16, features=2, log2_table_size=19, mlp_hidden_layers=3)
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def gen_local(kind, gdims, lo, hi, dev, tau=0.35, dtype=torch.float64):
+    """The analytic field on the node box [lo, hi] (x, y, z inclusive), [z][y][x] fp32."""
+    out = torch.empty((hi[2] - lo[2] + 1, hi[1] - lo[1] + 1, hi[0] - lo[0] + 1), dtype=torch.float32, device=dev)
+    for z0 in range(0, out.shape[0], 8):
+        z1 = min(z0 + 8, out.shape[0])
+        pos = synth.lattice(gdims, dev, (lo[2] + z0, lo[2] + z1))[:, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+        out[z0:z1] = synth.evaluate(kind, pos.to(dtype), gdims, tau=tau).to(torch.float32)
+    return out
+
+
+def fit_and_measure(d, vol, steps, batch, bb, stream):
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = bb
+    d.fit(vol, 2, batch, opts, stream, report=True)          # warm-up (2 steps)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    reps = d.fit(vol, steps - 2, batch, opts, stream, report=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    coords = len(d.models) * (batch + bb) * (steps - 2)   # every block of these configs has an interior face
+    return ms, coords, reps
+
+
+def psnr_1x(d, vol, stream):
+    out = torch.empty_like(vol)
+    sse = torch.zeros(1, dtype=torch.float64, device=vol.device)
+    d.decode_grid_local(out, 1, None, None, stream)          # warm
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    d.decode_grid_local(out, 1, vol, sse, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    lo, hi = d.core_box()
+    n = 1
+    for a in range(3):
+        n *= hi[a] - lo[a] + 1
+    return d.psnr(float(sse.item()), n), e0.elapsed_time(e1), n
+
+
+def ratio(d, n_core):
+    return 4.0 * n_core / d.param_bytes()
+
+
+def run_cfg1(stream, prec):
+    n = 64
+    dev = torch.device("cuda")
+    cfg = inr.make_config(levels=8, features=2, log2_table_size=14, mlp_hidden_layers=2, precision=prec)
+    d = dnr.DNR((n, n, n), (n, n, n), cfg)
+    vol = synth.g1_analytic(n, device=dev)
+    d.value_range(vol, stream)
+    ms, coords, _ = fit_and_measure(d, vol, 200, 4096, 0, stream)
+    p, dms, nvox = psnr_1x(d, vol, stream)
+    r = {"config": "cfg1", "precision": "fp16" if prec else "fp32", "fit_coords_per_s": coords / (ms / 1e3),
+         "fit_ms_per_step": ms / 198, "decode_voxels_per_s": nvox / (dms / 1e3), "psnr_db": p,
+         "steps": 200, "compression_ratio": ratio(d, n ** 3)}
+    d.close()
+    return r
+
+
+def run_cfg2(stream, prec):
+    n = 256
+    dev = torch.device("cuda")
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
+    vol = gen_local("g2", (n, n, n), d.lo, d.hi, dev)
+    d.value_range(vol, stream)
+    ms, coords, _ = fit_and_measure(d, vol, 2000, 65536, 16384, stream)
+    p, dms, nvox = psnr_1x(d, vol, stream)
+    r = {"config": "cfg2", "precision": "fp16" if prec else "fp32", "fit_coords_per_s": coords / (ms / 1e3),
+         "fit_ms_per_step": ms / 1998, "decode_voxels_per_s": nvox / (dms / 1e3), "psnr_db": p,
+         "steps": 2000, "compression_ratio": ratio(d, n ** 3)}
+    d.close()
+    return r
+
+
+def run_cfg3(stream, prec):
+    """512^3 G3, 64 blocks on one GPU, cfg2 network, 1000 steps; decode 1x and 2x
+    (2x against the analytic field)."""
+    n = 512
+    dev = torch.device("cuda")
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
+    vol = gen_local("g3", (n, n, n), d.lo, d.hi, dev)
+    d.value_range(vol, stream)
+    ms, coords, _ = fit_and_measure(d, vol, 1000, 65536, 16384, stream)
+    p1, dms1, nvox = psnr_1x(d, vol, stream)
+    # 2x: decode z-slabs of blocks at scale 2 and compare with the analytic field at (k + j/2)
+    sse2, n2, dms2 = 0.0, 0, 0.0
+    rng = (d.vmax - d.vmin)
+    for bz in range(4):
+        ids = [b for b in d.block_ids if dnr.block_origin(b, d.global_dims, d.n)[2] == bz * 128]
+        out = torch.empty((256, 1024, 1024), dtype=torch.float32, device=dev)
+        e0, e1 = ev(), ev()
+        e0.record()
+        for b in ids:
+            m = d.models[d.block_ids.index(b)]
+            o = dnr.block_origin(b, d.global_dims, d.n)
+            base = out[:, 2 * o[1]:, 2 * o[0]:]
+            inr.inr_decode_grid(m, (256, 256, 256), base.data_ptr(), (1, 1024, 1024 * 1024), None, None, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        dms2 += e0.elapsed_time(e1)
+        for z0 in range(0, 256, 16):
+            zs = (torch.arange(z0, z0 + 16, device=dev, dtype=torch.float32) / 2 + bz * 128)
+            ys = torch.arange(1024, device=dev, dtype=torch.float32) / 2
+            xs = torch.arange(1024, device=dev, dtype=torch.float32) / 2
+            zz, yy, xx = torch.meshgrid(zs, ys, xs, indexing="ij")
+            pos = torch.stack([xx, yy, zz], -1).clamp(max=float(n - 1))
+            truth = synth.evaluate("g3", pos, (n, n, n)).to(torch.float32)
+            sse2 += float((((out[z0:z0 + 16].double() - truth.double()) / rng) ** 2).sum())
+            n2 += truth.numel()
+        del out
+    p2 = -10 * math.log10(sse2 / n2) if sse2 > 0 else 200.0
+    r = {"config": "cfg3", "precision": "fp16" if prec else "fp32", "blocks": len(d.models),
+         "fit_coords_per_s": coords / (ms / 1e3), "fit_ms_per_step": ms / 998, "steps": 1000,
+         "decode_1x_voxels_per_s": nvox / (dms1 / 1e3), "psnr_1x_db": p1,
+         "decode_2x_voxels_per_s": n2 / (dms2 / 1e3), "psnr_2x_db_vs_analytic": p2,
+         "compression_ratio": ratio(d, n ** 3)}
+    d.close()
+    return r
+
+
+def run_cfg4(stream, prec, timesteps=100, window=40, steps=500):
+    """Temporal cache: per timestep of an evolving G2 256^3
+    field, reset + fit 500 steps, insert into a window of 40 (FIFO evicts);
+    every 10th insert decodes a random cached timestep at 256^3."""
+    n = 256
+    dev = torch.device("cuda")
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
+    cache = inr.cache_create(window, 0, 0)
+    rs = np.random.default_rng(4)
+    fit_ms, psnrs, bytes_curve, trig = [], [], [], []
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = 16384
+    vols = {}
+    for ti in range(timesteps):
+        tau = ti / timesteps
+        vol = gen_local("g2", (n, n, n), d.lo, d.hi, dev, tau=tau)
+        d.value_range(vol, stream)
+        for m in d.models:
+            inr.inr_reset(m, 0x230410516 + ti)
+        e0, e1 = ev(), ev()
+        e0.record()
+        d.fit(vol, steps, 65536, opts, stream, report=True)
+        e1.record()
+        torch.cuda.synchronize()
+        fit_ms.append(e0.elapsed_time(e1))
+        ev_ts = inr.cache_insert(cache, ti, d.models, stream)
+        bytes_curve.append(inr.cache_bytes(cache))
+        vols[ti] = vol
+        if ev_ts >= 0:
+            vols.pop(ev_ts, None)
+        if ti % 10 == 9:
+            k = int(rs.integers(0, inr.cache_size(cache)))
+            ts, blocks = inr.cache_get(cache, k)
+            out = torch.empty((n, n, n), device=dev)
+            sse = torch.zeros(1, dtype=torch.float64, device=dev)
+            e0, e1 = ev(), ev()
+            e0.record()
+            for b, bid in zip(blocks, d.block_ids):
+                o = dnr.block_origin(bid, d.global_dims, d.n)
+                inr.inr_decode_grid(b, (128, 128, 128), out[o[2]:, o[1]:, o[0]:].data_ptr(), (1, n, n * n),
+                                    vols[ts][o[2]:, o[1]:, o[0]:].data_ptr() if ts in vols else None,
+                                    sse.data_ptr() if ts in vols else None, stream)
+            e1.record()
+            torch.cuda.synchronize()
+            tr = {"insert": ti, "decoded_timestep": ts, "decode_ms": e0.elapsed_time(e1)}
+            if ts in vols:
+                tr["psnr_db"] = -10 * math.log10(float(sse.item()) / n ** 3)
+            trig.append(tr)
+        # PSNR of the fresh model on its own timestep
+        p, _, _ = psnr_1x(d, vol, stream)
+        psnrs.append(p)
+    r = {"config": "cfg4", "precision": "fp16" if prec else "fp32", "timesteps": timesteps, "window": window,
+         "steps_per_insert": steps, "fit_ms_per_insert_mean": float(np.mean(fit_ms)),
+         "fit_coords_per_s": 8 * (65536 + 16384) * steps / (np.mean(fit_ms) / 1e3),
+         "psnr_db_mean": float(np.mean(psnrs)), "psnr_db_min": float(np.min(psnrs)),
+         "cache_bytes_final": bytes_curve[-1], "cache_bytes_max": max(bytes_curve),
+         "cache_bytes_curve_every10": bytes_curve[::10], "evictions": timesteps - window,
+         "triggers": trig, "compression_ratio": ratio(d, n ** 3),
+         "raw_bytes_window": window * 4 * n ** 3}
+    inr.cache_destroy(cache)
+    d.close()
+    return r
+
+
+def run_cfg5(stream, prec):
+    """One GPU's share of cfg5: 64 of the 512 blocks (a 1024 x 1024 x 128 slab), T = 2^22,
+    200 fit steps just to get a model, then a query-throughput sweep 2^10 .. 2^26 over
+    the slab (block-bucketed), and the slab's 1x grid decode."""
+    n = 1024
+    dev = torch.device("cuda")
+    net = dict(NET2, log2_table_size=22)
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **net), rank=0, world=8)
+    vol = gen_local("g3", (n, n, n), d.lo, d.hi, dev)
+    d.value_range(vol, stream)     # (one GPU: its own range; the 8-GPU run all-reduces)
+    ms, coords, _ = fit_and_measure(d, vol, 200, 65536, 16384, stream)
+    p, dms, nvox = psnr_1x(d, vol, stream)
+    sweep = []
+    lo, hi = d.core_box()
+    span = torch.tensor([hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]], device=dev, dtype=torch.float32)
+    base = torch.tensor(lo, device=dev, dtype=torch.float32)
+    for e in range(10, 27, 2):
+        q = 1 << e
+        g = torch.Generator(device=dev)
+        g.manual_seed(e)
+        pts = torch.rand((q, 3), device=dev, generator=g) * span + base
+        out = torch.empty(q, device=dev)
+        inr.inr_decode_group(d.models, pts.data_ptr(), q, out.data_ptr(), 0, stream)
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        reps = 3
+        for _ in range(reps):
+            inr.inr_decode_group(d.models, pts.data_ptr(), q, out.data_ptr(), 0, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        sweep.append({"queries": q, "ms": t, "queries_per_s": q / (t / 1e3)})
+        del pts, out
+    r = {"config": "cfg5 (one GPU's 64 of 512 blocks)", "precision": "fp16" if prec else "fp32",
+         "blocks": len(d.models), "fit_coords_per_s": coords / (ms / 1e3), "fit_ms_per_step": ms / 198,
+         "steps": 200, "decode_1x_voxels_per_s": nvox / (dms / 1e3), "psnr_1x_db": p,
+         "query_sweep": sweep, "compression_ratio": ratio(d, 128 ** 3 * len(d.models)),
+         "param_bytes_gpu": d.param_bytes()}
+    d.close()
+    return r
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5")
+    ap.add_argument("--precision", default="fp16,fp32")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_configs.json"))
+    a = ap.parse_args()
+    torch.cuda.set_stream(torch.cuda.Stream())
+    stream = torch.cuda.current_stream().cuda_stream
+    fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5}
+    results = []
+    for name in a.only.split(","):
+        for p in a.precision.split(","):
+            prec = inr.INR_PREC_FP16_MLP if p == "fp16" else inr.INR_PREC_FP32
+            if name in ("cfg3", "cfg4", "cfg5") and p == "fp32":
+                continue          # the fp32 CUDA-core path is the parity mode; large configs run fp16
+            t0 = time.time()
+            r = fns[name](stream, prec)
+            r["wall_s"] = time.time() - t0
+            print(json.dumps(r), flush=True)
+            results.append(r)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump({"gpu": torch.cuda.get_device_name(0), "results": results}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

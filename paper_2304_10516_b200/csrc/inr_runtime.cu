@@ -340,6 +340,7 @@ extern "C" inr_status inr_reset(inr_model* m, uint64_t seed) {
   if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
   if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
   CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());   // work queued on any stream may still use the parameters
   m->cfg.seed = seed;
   inr_status s = init_state(m, seed, 0);
   if (s) return s;
