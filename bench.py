@@ -247,6 +247,19 @@ def run_ours(args):
     roof["avg_launch_ms"] = avg_s * 1e3
     roof["share_of_step"] = dom_ms / ms
     kernels = {k: {"total_ms": v[0], "launches": v[1], "avg_ms": v[0] / max(v[1], 1)} for k, v in kern.items()}
+    # the gather / scatter kernels against the measured random-access peaks (tools/l2_peaks.py)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_l2_peaks.json")) as f:
+            lp = {(r["op"], r["buffer_MB"]): r["per_s"] for r in json.load(f)["results"]}
+        corners = 8.0 * CFG["levels"] * coords_per_step
+        for k, op in (("encode_fwd", "gather_16B"), ("encode_bwd", "red_v4_f32")):
+            if k in kernels:
+                rate = corners / (kernels[k]["avg_ms"] / 1e3)
+                kernels[k].update({"corner_accesses_per_s": rate, "random_access_peak_per_s": lp[(op, 4)],
+                                   "peak_note": f"{op}, 4 MB L2-resident buffer, measured; x-neighbour corner "
+                                                "pairs share one access, so corners/s can exceed the access peak"})
+    except (OSError, KeyError, ValueError):
+        pass
 
     # ---- end to end through the public API with host buffers: every step the
     # volume is copied H2D from pinned memory, one fit step runs through
