@@ -447,6 +447,19 @@ static inr_status validate_view(const inr_model* m, const inr_view* v) {
   return INR_OK;
 }
 
+// Keep stream-ordered workspace allocations in the device's pool between calls
+// (the default release threshold of 0 unmaps them at every synchronization).
+static void keep_pool(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 static inr_status fit_impl(inr_model* const* models, const inr_view* views, int32_t nmodels, int32_t steps,
                            int32_t batch, const inr_fit_opts* opts, inr_fit_report* out, cudaStream_t st) {
   if (!models || !views || nmodels < 1) return fail(INR_ERR_INVALID_ARG, "models/views missing");
@@ -467,6 +480,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   }
   const inr_model* m0 = models[0];
   CK(cudaSetDevice(m0->device));
+  keep_pool(m0->device);
   const bool tc = m0->cfg.precision == INR_PREC_FP16_MLP;
   if (tc && !tc_supported(m0->net)) return fail(INR_ERR_UNSUPPORTED, "configuration not supported by the tcgen05 MLP");
 
@@ -667,6 +681,7 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
   const inr_model* m0 = models[0];
   if (!m0) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
   CK(cudaSetDevice(m0->device));
+  keep_pool(m0->device);
   QueryArgs* qa = new QueryArgs();
   memset(qa, 0, sizeof *qa);
   qa->net = m0->net;
