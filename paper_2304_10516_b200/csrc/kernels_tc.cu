@@ -171,9 +171,12 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
 
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
+  // dW_H / db_H partial sums of this CTA: fp32, or exact int64 fixed point in the
+  // deterministic mode (the 4 warps add in a run-dependent order)
   float* red = reinterpret_cast<float*>(smem + lay.red);
+  unsigned long long* redx = reinterpret_cast<unsigned long long*>(smem + lay.red);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  for (int i = t; i < 66; i += kThreads) red[i] = 0.f;
+  for (int i = t; i < 66; i += kThreads) redx[i] = 0ull;
   const uint32_t tmem = mlp_setup_fit(net, wimg + (size_t)m * lay.img_bytes, smem, lay);
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0;
@@ -272,12 +275,20 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
       warp_transpose_reduce64(v, lane);
       int c0 = ((lane >> 4) & 1) * 32 + ((lane >> 3) & 1) * 16 + ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 +
                (lane & 1) * 2;
-      atomicAdd(red + c0, v[0]);
-      atomicAdd(red + c0 + 1, v[1]);
+      if (GX) {
+        atomicAdd(redx + c0, (unsigned long long)__double2ll_rn((double)v[0] * (double)(1ll << kFixedShift)));
+        atomicAdd(redx + c0 + 1, (unsigned long long)__double2ll_rn((double)v[1] * (double)(1ll << kFixedShift)));
+      } else {
+        atomicAdd(red + c0, v[0]);
+        atomicAdd(red + c0 + 1, v[1]);
+      }
       float s = dy;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) atomicAdd(red + 64, s);
+      if (lane == 0) {
+        if (GX) atomicAdd(redx + 64, (unsigned long long)__double2ll_rn((double)s * (double)(1ll << kFixedShift)));
+        else atomicAdd(red + 64, s);
+      }
     }
     // dz_{H-1} = dy W_H * 1[z_{H-1} > 0], scaled by 2^s
     {
@@ -375,8 +386,13 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
   }
   __syncthreads();
   if (!first) {
-    for (int n = t; n < 64; n += kThreads) grad_add(G, GX, net.w_off[H] + n, red[n]);
-    if (t == 0 && net.bias) grad_add(G, GX, net.b_off[H], red[64]);
+    if (GX) {
+      for (int n = t; n < 64; n += kThreads) atomicAdd(GX + net.w_off[H] + n, redx[n]);
+      if (t == 0 && net.bias) atomicAdd(GX + net.b_off[H], redx[64]);
+    } else {
+      for (int n = t; n < 64; n += kThreads) atomicAdd(G + net.w_off[H] + n, red[n]);
+      if (t == 0 && net.bias) atomicAdd(G + net.b_off[H], red[64]);
+    }
   }
   mlp_teardown(tmem, lay);
 }
@@ -413,7 +429,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   if (train) L.h0b = take(L.feat_tile_bytes, 1024);
   L.dz_sbo = 8 * 128;
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
-  L.red = take(66 * 4, 16);
+  L.red = take(66 * 8, 16);
   L.mbar = take(8, 8);
   L.mbar_img = take(8, 8);
   L.mbar_feat[0] = take(8, 8);

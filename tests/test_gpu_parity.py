@@ -203,7 +203,8 @@ def test_forward_fp16_tensor_core_2e3():
         inr.inr_destroy(m)
 
 
-def test_deterministic_mode_bitwise_reproducible():
+@pytest.mark.parametrize("prec", [0, 1])
+def test_deterministic_mode_bitwise_reproducible(prec):
     vol = synth.g1_analytic(32).numpy()
     blk = sampler.decompose((32, 32, 32), (16, 16, 16))[0]
     vt = gpu_volume(vol)
@@ -211,7 +212,7 @@ def test_deterministic_mode_bitwise_reproducible():
     go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 256
     out = []
     for _ in range(2):
-        m = make_gpu_model(blk, 5, reduction=1, **CFG1)
+        m = make_gpu_model(blk, 5, reduction=1, precision=prec, **CFG1)
         inr.inr_fit(m, whole_view(vt), 5, 1024, go, stream())
         out.append((get_params(m), get_grads(m)))
         inr.inr_destroy(m)
@@ -359,7 +360,8 @@ def test_cache_fifo_and_decode_from_slot(host):
     inr.inr_destroy(m)
 
 
-def test_group_fit_matches_single_fits():
+@pytest.mark.parametrize("prec", [0, 1])
+def test_group_fit_matches_single_fits(prec):
     """Blocks are independent: a grouped launch gives each model
     the same result as fitting it alone (deterministic mode, bitwise)."""
     vol = synth.g2_energy(32).numpy()
@@ -367,10 +369,10 @@ def test_group_fit_matches_single_fits():
     vt = gpu_volume(vol)
     go = inr.inr_fit_opts_default()
     go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
-    group = [make_gpu_model(b, 6, reduction=1, **CFG1) for b in blocks]
+    group = [make_gpu_model(b, 6, reduction=1, precision=prec, **CFG1) for b in blocks]
     reps = inr.inr_fit_group(group, [whole_view(vt)] * len(group), 6, 256, go, stream())
     assert all(r.steps_taken == 6 for r in reps)
-    single = make_gpu_model(blocks[6], 6, reduction=1, **CFG1)
+    single = make_gpu_model(blocks[6], 6, reduction=1, precision=prec, **CFG1)
     inr.inr_fit(single, whole_view(vt), 6, 256, go, stream())
     assert np.array_equal(get_params(single), get_params(group[6]))
     for m in group + [single]:
