@@ -420,10 +420,18 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   L.wout = take(68 * 4, 16);
   L.img_bytes = (off + 15) / 16 * 16;
   off = L.img_bytes;
-  for (int k = 0; k < net.H; ++k) {
-    int in = net.in_dim[k];
-    L.h_sbo[k] = (uint32_t)((in + L.ones) / 8) * 128;
-    L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
+  if (train) {   // every activation tile is kept for the backward pass
+    for (int k = 0; k < net.H; ++k) {
+      int in = net.in_dim[k];
+      L.h_sbo[k] = (uint32_t)((in + L.ones) / 8) * 128;
+      L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
+    }
+  } else {       // forward only: two ping-pong buffers (layer k reads one, its epilogue writes the other)
+    const uint32_t hb[2] = {take(kTileM * 64 * 2, 1024), take(kTileM * 64 * 2, 1024)};
+    for (int k = 0; k < net.H; ++k) {
+      L.h_sbo[k] = (uint32_t)(net.in_dim[k] / 8) * 128;
+      L.h[k] = hb[k & 1];
+    }
   }
   L.feat_tile_bytes = kTileM * (net.LF + L.ones) * 2;
   if (train) L.h0b = take(L.feat_tile_bytes, 1024);
@@ -531,7 +539,7 @@ struct FwdArgs {
 };
 
 template <int F, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
+__global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -599,26 +607,28 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(GroupArgs g, Fw
       }
     }
     {
-      float f[64];
+      // features straight into this thread's row of the h_0 tile (no staging array)
+      uint8_t* row = smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0];
+#pragma unroll 1
+      for (int l = 0; l < net.L; ++l) {
+        float fl[F];
+        if (MODE == 0) encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+        else encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
+        const int c = l * F;
+        if constexpr (F == 1) {
+          *reinterpret_cast<__half*>(row + (c >> 3) * 128 + (c & 7) * 2) = __float2half_rn(fl[0]);
+        } else {
 #pragma unroll
-      for (int l = 0; l < kMaxLevels; ++l) {
-        if (l < net.L) {
-          float fl[F];
-          if (MODE == 0) encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
-          else encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
-#pragma unroll
-          for (int jj = 0; jj < F; ++jj)
-            if (l * F + jj < 64) f[l * F + jj] = fl[jj];
+          for (int jj = 0; jj < F; jj += 2)
+            *reinterpret_cast<__half2*>(row + ((c + jj) >> 3) * 128 + ((c + jj) & 7) * 2) =
+                __floats2half2_rn(fl[jj], fl[jj + 1]);
         }
       }
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-        if (jj * 8 < LF) st_row8(smem + lay.h[0], lay.h_sbo[0], t, jj, f + 8 * jj);
     }
     fence_async_smem();
     fence_before();
     __syncthreads();
-    float hH[64];
+    float y = wout[64];
     for (int k = 0; k < H; ++k) {
       if (t == 0) {
         fence_after();
@@ -644,17 +654,14 @@ __global__ void __launch_bounds__(kThreads, 1) forward_tc_kernel(GroupArgs g, Fw
       if (k + 1 < H) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, jj, z + 8 * jj);
-      } else {
+      } else {   // the 64 -> 1 output layer, fp32 on CUDA cores
 #pragma unroll
-        for (int n = 0; n < 64; ++n) hH[n] = z[n];
+        for (int n = 0; n < 64; ++n) y = fmaf(wout[n], z[n], y);
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
-    float y = wout[64];
-#pragma unroll
-    for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
     if constexpr (MODE == 0) {
       if (valid) a.y[j] = y;
     } else {
