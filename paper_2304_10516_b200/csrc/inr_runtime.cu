@@ -617,10 +617,13 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   bool nonfinite = false;
   for (int i = 0; i < nmodels; ++i) {
     const inr_model* m = models[i];
+    // one copy per model: acc[0..2] (doubles at +16) and the flag (int at +48) are adjacent
+    unsigned char tail[40];
+    CK(cudaMemcpy(tail, m->acc, sizeof tail, cudaMemcpyDeviceToHost));
     double acc[2];
     int flag = 0;
-    CK(cudaMemcpy(acc, m->acc, sizeof acc, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&flag, m->flag, sizeof flag, cudaMemcpyDeviceToHost));
+    memcpy(acc, tail, sizeof acc);
+    memcpy(&flag, tail + 32, sizeof flag);
     inr_fit_report& r = out[i];
     r.steps_taken = taken;
     r.reached_target = reached[i];
