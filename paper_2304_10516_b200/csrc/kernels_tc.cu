@@ -145,26 +145,53 @@ __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
 
 // ---------------------------------------------------------------------------
 // MLP forward + Eq. 2 + backward on tensor cores for level-major features
-// (the middle kernel of the fp16 fit pipeline).  feat: fp16 [model][level][Bs][F],
-// samples: float4 (x, y, z, target) [model][Bs]; writes dfeat fp32
-// [model][level][Bs][F]; adds dW, db into the model's gradient.
+// (the middle kernel of the fp16 fit pipeline).  256 threads: thread t owns
+// row r = t % 128 of the tile (TMEM lane r) and column half t / 128 (32 of the
+// 64 columns), so every epilogue is split across two threads and twice as many
+// warps hide the MMA and TMEM latencies.  featimg: fp16 h_0 tile images,
+// samples: float4 (x, y, z, target); writes dfeat fp32 [model][level][Bs][F];
+// adds dW, db into the model's gradient.
+constexpr int kFitThreads = 256;
+
+// Sum 32 per-lane values over the warp; lane l ends with the sum of column l.
+__device__ __forceinline__ float warp_transpose_reduce32(float* v, int lane) {
+#pragma unroll
+  for (int half = 16, off = 16; off >= 1; half >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      float keep = up ? v[j + half] : v[j];
+      float send = up ? v[j] : v[j + half];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+__device__ __forceinline__ void red_smem(float* red, unsigned long long* redx, bool det, int i, float v) {
+  if (det) atomicAdd(redx + i, (unsigned long long)__double2ll_rn((double)v * (double)(1ll << kFixedShift)));
+  else atomicAdd(red + i, v);
+}
+
 template <int F>
-__global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitScalars fs, Layout lay,
-                                                             float loss_scale, const uint8_t* __restrict__ featimg,
-                                                             const uint8_t* __restrict__ wimg,
-                                                             const float4* __restrict__ samples,
-                                                             float* __restrict__ dfeat, int Bs) {
+__global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, FitScalars fs, Layout lay,
+                                                                float loss_scale, const uint8_t* __restrict__ featimg,
+                                                                const uint8_t* __restrict__ wimg,
+                                                                const float4* __restrict__ samples,
+                                                                float* __restrict__ dfeat, int Bs) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
   const int m = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int r = t & (kTileM - 1), hf = t >> 7, cb = hf * 32;   // row, column half
   const int H = net.H, L = net.L, ones = lay.ones;
   const int B_b = md.nfaces > 0 ? fs.B_b : 0;
   const int total = fs.B_u + B_b;
   const int ntiles = (total + kTileM - 1) / kTileM;
   float* __restrict__ G = md.grads;
   unsigned long long* __restrict__ GX = md.grads_fx;
+  const bool det = GX != nullptr;
   const float inv_scale = 1.f / loss_scale;
   const uint8_t* featm = featimg + (size_t)m * (Bs / kTileM) * lay.feat_tile_bytes;
   float* dfeatm = dfeat + (size_t)m * L * Bs * F;
@@ -172,13 +199,14 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
   // dW_H / db_H partial sums of this CTA: fp32, or exact int64 fixed point in the
-  // deterministic mode (the 4 warps add in a run-dependent order)
+  // deterministic mode (the warps add in a run-dependent order)
   float* red = reinterpret_cast<float*>(smem + lay.red);
   unsigned long long* redx = reinterpret_cast<unsigned long long*>(smem + lay.red);
+  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [2][128] output-layer partial sums
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  for (int i = t; i < 66; i += kThreads) redx[i] = 0ull;
+  for (int i = t; i < 66; i += kFitThreads) redx[i] = 0ull;
   const uint32_t tmem = mlp_setup_fit(net, wimg + (size_t)m * lay.img_bytes, smem, lay);
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   uint32_t phase = 0;
   bool first = true;
   const float lam = B_b > 0 ? fs.lambda : 0.f;
@@ -191,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
 
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int i = tile * kTileM + t;
+    const int i = tile * kTileM + r;
     const bool valid = i < total;
     const bool is_b = i >= fs.B_u;
     const float target = valid ? samples[(size_t)m * Bs + i].w : 0.f;
@@ -203,9 +231,9 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
                fbar[b ^ 1]);
     }
     mbar_wait(fbar[b], (uint32_t)(it >> 1) & 1u);
-    // ---- forward through the hidden layers
-    uint32_t mask[kMaxLayers][2];
-    float hH[64];
+    // ---- forward through the hidden layers (this thread: columns [cb, cb + 32))
+    uint32_t mask[kMaxLayers];
+    float hH[32];
     for (int k = 0; k < H; ++k) {
       const int in = net.in_dim[k];
       if (t == 0) {
@@ -217,44 +245,45 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
       mbar_wait(mbar, phase);
       phase ^= 1;
       fence_after();
-      float z[64];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_base + c * 16, z + c * 16);
+      float z[32];
+      tmem_ld16(tmem + lane_base + cb, z);
+      tmem_ld16(tmem + lane_base + cb + 16, z + 16);
       tmem_wait_ld();
-      uint32_t m0 = 0, m1 = 0;
+      uint32_t mk = 0;
 #pragma unroll
-      for (int n = 0; n < 64; n += 4) {
-        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + n);
-        z[n] += b4.x; z[n + 1] += b4.y; z[n + 2] += b4.z; z[n + 3] += b4.w;
-      }
+      for (int n = 0; n < 32; n += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + cb + n);
+        const float v[4] = {z[n] + b4.x, z[n + 1] + b4.y, z[n + 2] + b4.z, z[n + 3] + b4.w};
 #pragma unroll
-      for (int n = 0; n < 64; ++n) {
-        float v = z[n];
-        bool pos = v > 0.f && valid;
-        if (n < 32) m0 |= (uint32_t)pos << n; else m1 |= (uint32_t)pos << (n - 32);
-        z[n] = pos ? v : 0.f;
+        for (int q = 0; q < 4; ++q) {
+          const bool pos = v[q] > 0.f && valid;
+          mk |= (uint32_t)pos << (n + q);
+          z[n + q] = pos ? v[q] : 0.f;
+        }
       }
-      mask[k][0] = m0;
-      mask[k][1] = m1;
+      mask[k] = mk;
       if (k + 1 < H) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, j, z + 8 * j);
+        for (int j = 0; j < 4; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], r, hf * 4 + j, z + 8 * j);
       } else {
+        float yp = 0.f;
 #pragma unroll
-        for (int n = 0; n < 64; ++n) hH[n] = z[n];
+        for (int n = 0; n < 32; ++n) {
+          hH[n] = z[n];
+          yp = fmaf(wout[cb + n], z[n], yp);
+        }
+        ypart[hf * kTileM + r] = yp;
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
     // ---- output layer (fp32, CUDA cores) and Eq. 2
-    float y = wout[64];
-#pragma unroll
-    for (int n = 0; n < 64; ++n) y = fmaf(wout[n], hH[n], y);
+    const float y = wout[64] + ypart[r] + ypart[kTileM + r];
     const float d = y - target;
     const float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
     const float dy = is_b ? lam * sg / (float)max(B_b, 1) : (1.f - lam) * sg / (float)fs.B_u;
-    {
+    if (hf == 0) {
       double au = (valid && !is_b) ? fabs((double)d) : 0.0;
       double ab = (valid && is_b) ? fabs((double)d) : 0.0;
 #pragma unroll
@@ -266,41 +295,24 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
         if (au != 0.0) atomicAdd(md.acc + 0, au);
         if (ab != 0.0) atomicAdd(md.acc + 1, ab);
       }
-    }
-    // dW_H[n] = sum_s dy_s h_H[s][n], db_H = sum_s dy_s (warp transpose-reduce, then smem)
-    {
-      float v[64];
-#pragma unroll
-      for (int n = 0; n < 64; ++n) v[n] = dy * hH[n];
-      warp_transpose_reduce64(v, lane);
-      int c0 = ((lane >> 4) & 1) * 32 + ((lane >> 3) & 1) * 16 + ((lane >> 2) & 1) * 8 + ((lane >> 1) & 1) * 4 +
-               (lane & 1) * 2;
-      if (GX) {
-        atomicAdd(redx + c0, (unsigned long long)__double2ll_rn((double)v[0] * (double)(1ll << kFixedShift)));
-        atomicAdd(redx + c0 + 1, (unsigned long long)__double2ll_rn((double)v[1] * (double)(1ll << kFixedShift)));
-      } else {
-        atomicAdd(red + c0, v[0]);
-        atomicAdd(red + c0 + 1, v[1]);
-      }
       float s = dy;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) {
-        if (GX) atomicAdd(redx + 64, (unsigned long long)__double2ll_rn((double)s * (double)(1ll << kFixedShift)));
-        else atomicAdd(red + 64, s);
-      }
+      if (lane == 0) red_smem(red, redx, det, 64, s);               // db_H
     }
-    // dz_{H-1} = dy W_H * 1[z_{H-1} > 0], scaled by 2^s
-    {
-      float dz[64];
+    {   // dW_H[n] = sum_s dy_s h_H[s][n] for this thread's 32 columns
+      float v[32];
+#pragma unroll
+      for (int n = 0; n < 32; ++n) v[n] = dy * hH[n];
+      red_smem(red, redx, det, cb + lane, warp_transpose_reduce32(v, lane));
+    }
+    {   // dz_{H-1} = dy W_H * 1[z_{H-1} > 0], scaled by 2^s
+      float dz[32];
       const float sdy = dy * loss_scale;
 #pragma unroll
-      for (int n = 0; n < 64; ++n) {
-        bool pos = ((n < 32 ? mask[H - 1][0] >> n : mask[H - 1][1] >> (n - 32)) & 1u) != 0;
-        dz[n] = pos ? sdy * wout[n] : 0.f;
-      }
+      for (int n = 0; n < 32; ++n) dz[n] = ((mask[H - 1] >> n) & 1u) ? sdy * wout[cb + n] : 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, t, j, dz + 8 * j);
+      for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dz + 8 * j);
     }
     fence_async_smem();
     fence_before();
@@ -323,32 +335,30 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
       mbar_wait(mbar, phase);
       phase ^= 1;
       fence_after();
-      float dh[64];
+      if (cb < in) {   // warp-uniform: this half has columns of dh
+        float dh[32];
+        tmem_ld16(tmem + lane_base + cb, dh);
+        tmem_ld16(tmem + lane_base + cb + 16, dh + 16);
+        tmem_wait_ld();
+        if (k > 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c * 16 < in) tmem_ld16(tmem + lane_base + c * 16, dh + c * 16);
-      tmem_wait_ld();
-      if (k > 0) {
+          for (int n = 0; n < 32; ++n) dh[n] = ((mask[k - 1] >> n) & 1u) ? dh[n] : 0.f;
 #pragma unroll
-        for (int n = 0; n < 64; ++n) {
-          bool pos = ((n < 32 ? mask[k - 1][0] >> n : mask[k - 1][1] >> (n - 32)) & 1u) != 0;
-          dh[n] = pos ? dh[n] : 0.f;
-        }
+          for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dh + 8 * j);
+        } else if (valid) {
+          // dfeat, unscaled, level-major (coalesced across the tile)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, t, j, dh + 8 * j);
-      } else if (valid) {
-        // dfeat, unscaled, level-major (coalesced across the tile)
+          for (int c = 0; c < 32; c += F) {
+            if (cb + c < net.LF) {
+              float* o = dfeatm + ((size_t)((cb + c) / F) * Bs + i) * F;
+              if constexpr (F == 1) { o[0] = dh[c] * inv_scale; }
+              else if constexpr (F == 2) { *reinterpret_cast<float2*>(o) = make_float2(dh[c] * inv_scale, dh[c + 1] * inv_scale); }
+              else {
 #pragma unroll
-        for (int c = 0; c < 64; c += F) {
-          if (c < net.LF) {
-            float* o = dfeatm + ((size_t)(c / F) * Bs + i) * F;
-            if constexpr (F == 1) { o[0] = dh[c] * inv_scale; }
-            else if constexpr (F == 2) { *reinterpret_cast<float2*>(o) = make_float2(dh[c] * inv_scale, dh[c + 1] * inv_scale); }
-            else {
-#pragma unroll
-              for (int q = 0; q < F; q += 4)
-                *reinterpret_cast<float4*>(o + q) = make_float4(dh[c + q] * inv_scale, dh[c + q + 1] * inv_scale,
-                                                                dh[c + q + 2] * inv_scale, dh[c + q + 3] * inv_scale);
+                for (int q = 0; q < F; q += 4)
+                  *reinterpret_cast<float4*>(o + q) = make_float4(dh[c + q] * inv_scale, dh[c + q + 1] * inv_scale,
+                                                                  dh[c + q + 2] * inv_scale, dh[c + q + 3] * inv_scale);
+              }
             }
           }
         }
@@ -366,13 +376,13 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
     for (int k = 0; k < H; ++k) {
       const int in = net.in_dim[k];
       const int ncol = in + ones;
-      // M = 64 accumulator: row 16w + r lives in lane 32w + r (r < 16)
-      for (int c = 0; c < ncol; c += 16) {
+      // M = 64 accumulator: row 16q + l lives in lane 32q + l (l < 16); halves take alternate 16-column chunks
+      for (int c = hf * 16; c < ncol; c += 32) {
         float v[16];
         tmem_ld16(tmem + lane_base + lay.col_dw[k] + c, v);
         tmem_wait_ld();
         if (lane < 16) {
-          const int n = warp * 16 + lane;
+          const int n = (warp & 3) * 16 + lane;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             int col = c + j;
@@ -386,11 +396,11 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_fit_kernel(GroupArgs g, FitSc
   }
   __syncthreads();
   if (!first) {
-    if (GX) {
-      for (int n = t; n < 64; n += kThreads) atomicAdd(GX + net.w_off[H] + n, redx[n]);
+    if (det) {
+      for (int n = t; n < 64; n += kFitThreads) atomicAdd(GX + net.w_off[H] + n, redx[n]);
       if (t == 0 && net.bias) atomicAdd(GX + net.b_off[H], redx[64]);
     } else {
-      for (int n = t; n < 64; n += kThreads) atomicAdd(G + net.w_off[H] + n, red[n]);
+      for (int n = t; n < 64; n += kFitThreads) atomicAdd(G + net.w_off[H] + n, red[n]);
       if (t == 0 && net.bias) atomicAdd(G + net.b_off[H], red[64]);
     }
   }
@@ -438,6 +448,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   L.dz_sbo = 8 * 128;
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
   L.red = take(66 * 8, 16);
+  L.ypart = take(2 * kTileM * 4, 16);
   L.mbar = take(8, 8);
   L.mbar_img = take(8, 8);
   L.mbar_feat[0] = take(8, 8);
@@ -507,7 +518,7 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
 #define CASE_F(FF)                                                                                   \
   case FF:                                                                                           \
     cudaFuncSetAttribute(mlp_fit_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
-    mlp_fit_kernel<FF><<<grid, kThreads, L.bytes, st>>>(g, fs, L, ls, featimg, wimg, samples, dfeat, Bs); \
+    mlp_fit_kernel<FF><<<grid, kFitThreads, L.bytes, st>>>(g, fs, L, ls, featimg, wimg, samples, dfeat, Bs); \
     break;
     CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
 #undef CASE_F
