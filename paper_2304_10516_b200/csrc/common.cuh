@@ -123,8 +123,10 @@ __device__ __forceinline__ float sample_target(const ModelDev& md, const float x
     r = fminf(fmaxf(r, 0.f), (float)(md.N[d] - 1));
     float fl = floorf(r);
     i0[d] = (int)fl;
-    i1[d] = min(i0[d] + 1, md.N[d] - 1);
     f[d] = __fsub_rn(r, fl);
+    // the upper node only when it has weight: on the block's far face (r = o + n)
+    // the view may end at node o + n (its contract), so node o + n + 1 must not be read
+    i1[d] = f[d] > 0.f ? min(i0[d] + 1, md.N[d] - 1) : i0[d];
   }
   float acc = 0.f;
 #pragma unroll

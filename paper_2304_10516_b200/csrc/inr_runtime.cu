@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <deque>
@@ -84,6 +85,10 @@ static void prof_record(cudaEvent_t e, cudaStream_t st) {
   else cudaEventRecord(e, st);
 }
 
+// INR_DEBUG_SYNC=1: synchronize after every library kernel and report the first
+// failing one by name on stderr (debugging aid; no effect otherwise).
+static const bool g_debug_sync = getenv("INR_DEBUG_SYNC") != nullptr;
+
 struct ProfScope {
   int kind;
   cudaStream_t st;
@@ -92,6 +97,11 @@ struct ProfScope {
     if (g_prof_on) { a = prof_event(); prof_record(a, st); }
   }
   ~ProfScope() {
+    if (g_debug_sync) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) fprintf(stderr, "[libinr] kernel %s failed: %s\n", kProfNames[kind], cudaGetErrorString(e));
+    }
     if (a) {
       cudaEvent_t b = prof_event();
       prof_record(b, st);

@@ -547,6 +547,7 @@ struct FwdArgs {
   const int* perm;
   const int* tile_slot;
   const int* ntiles_dev;
+  const uint8_t* wimg;   // prepared weight images, one per model slot (prep_image_kernel)
 };
 
 template <int F, int MODE>
@@ -554,38 +555,48 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int H = net.H, LF = net.LF;
+  const int H = net.H;
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  int cur = MODE == 2 ? -1 : 0;  // model whose weights are in smem
-  const uint32_t tmem = mlp_setup(net, g.md[0].params, smem, lay, false);
+  const uint32_t mbar_img = smem_u32(smem + lay.mbar_img);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(lay.ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (t == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar_img, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  uint32_t phase = 0;
+  uint32_t phase = 0, img_phase = 0;
+  int cur = -1;  // model whose weight image is in smem
+  // tiles are visited grid-stride: the CTAs in flight work on consecutive tiles,
+  // i.e. (MODE 2, tiles grouped by block) on one or two blocks' tables at a time;
+  // a CTA reloads weights only when its next tile belongs to another block
   long long ntiles;
   if constexpr (MODE == 0) ntiles = (a.q + kTileM - 1) / kTileM;
   else if constexpr (MODE == 1) ntiles = ((long long)a.res[0] * a.res[1] * a.res[2] + kTileM - 1) / kTileM;
   else ntiles = *a.ntiles_dev;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    int slot = 0;
-    if constexpr (MODE == 2) {
-      slot = a.tile_slot[tile];
-      if (slot != cur) {  // reload this block's weights (tiles are grouped by block)
-        __syncthreads();
-        const float* P = g.md[slot].params;
-        for (int k = 0; k < H; ++k) {
-          const int in = net.in_dim[k];
-          for (int e = t; e < 64 * in; e += kThreads) {
-            int n = e / in, i = e - n * in;
-            *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) =
-                __float2half_rn(P[net.w_off[k] + e]);
-          }
-          for (int n = t; n < 64; n += kThreads) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
-        }
-        for (int i = t; i < 64; i += kThreads) wout[i] = P[net.w_off[H] + i];
-        if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
-        cur = slot;
+  const long long t0 = blockIdx.x, t1 = ntiles, tstep = gridDim.x;
+  for (long long tile = t0; tile < t1; tile += tstep) {
+    const int slot = MODE == 2 ? a.tile_slot[tile] : 0;
+    if (slot != cur) {   // one TMA bulk copy of this block's prepared weight image
+      __syncthreads();
+      if (t == 0) {
+        mbar_expect_tx(mbar_img, lay.img_bytes);
+        bulk_g2s(smem_u32(smem), a.wimg + (size_t)slot * lay.img_bytes, lay.img_bytes, mbar_img);
       }
+      mbar_wait(mbar_img, img_phase);
+      img_phase ^= 1;
+      cur = slot;
     }
     const ModelDev& md = g.md[slot];
     const float* P = md.params;
@@ -696,9 +707,15 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
 }
 
 template <int MODE>
-static void launch_forward(const GroupArgs& g, const FwdArgs& a, long long ntiles_hint, cudaStream_t st) {
+static void launch_forward(const GroupArgs& g, const FwdArgs& a0, long long ntiles_hint, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L, false)) return;
+  FwdArgs a = a0;
+  uint8_t* wimg = nullptr;   // the models' fp16 weight images (stream-ordered scratch)
+  if (cudaMallocAsync((void**)&wimg, (size_t)g.nmodels * L.img_bytes, st) != cudaSuccess) return;
+  a.wimg = wimg;
+  prep_image_kernel<<<dim3(g.nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg);
+  count_launch();
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles_hint, 148ll * L.ctas_per_sm));
   switch (g.net.F) {
 #define CASE_F(FF)                                                                                              \
@@ -711,6 +728,7 @@ static void launch_forward(const GroupArgs& g, const FwdArgs& a, long long ntile
     default: break;
   }
   count_launch();
+  cudaFreeAsync(wimg, st);
 }
 
 static GroupArgs* single_group(const NetDesc& net, const ModelDev& md) {

@@ -458,3 +458,27 @@ def test_decode_tensor_core_fp16_models():
     assert normwise(rq.cpu().numpy(), o_decode.decode_query(oms, rp)) <= 2e-3
     for m in gms:
         inr.inr_destroy(m)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_view_is_read_only_inside_its_contract(prec):
+    """A block's view need only cover nodes [o, min(o+n, N-1)] (inr.h): embed the
+    17^3 nodes of block 0 of a 32^3 volume in a NaN-filled buffer — samples on the
+    block's far faces (x = 1, weight 0 on the next node) must not touch the NaNs,
+    and the step equals the one on the full volume."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[0]        # faces +x, +y, +z
+    buf = torch.full((20, 20, 20), float("nan"), device="cuda")
+    buf[:17, :17, :17] = torch.from_numpy(vol[:17, :17, :17]).cuda()
+    view = inr.make_view(buf.data_ptr(), (0, 0, 0), (17, 17, 17), (1, 20, 400))
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 512
+    a = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    rep = inr.inr_fit(a, view, 2, 1024, go, stream())
+    assert np.isfinite(rep.loss_uniform) and np.isfinite(rep.loss_boundary)
+    b = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    vt = gpu_volume(vol)
+    inr.inr_fit(b, whole_view(vt), 2, 1024, go, stream())
+    assert np.array_equal(get_params(a), get_params(b))
+    inr.inr_destroy(a)
+    inr.inr_destroy(b)
