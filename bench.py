@@ -34,8 +34,8 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default="fp16", choices=["fp16", "fp32"])
     p.add_argument("--psnr-steps", type=int, default=2000, help="total fit steps before the PSNR report (0: skip)")
@@ -111,7 +111,8 @@ def workload_config(world, args):
 
 # ------------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi sampled every 20 ms; only samples stamped inside the timed region count."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -123,32 +124,39 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over samples with t0 <= stamp <= t1 (host time)."""
+        import datetime
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, n_all = [], None, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in out.strip().splitlines():
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
+            if len(f) < 8:
                 continue
+            n_all += 1
             try:
-                sm.append(float(f[0]))
-                smax = float(f[1])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if t0 is not None and not (t0 - 0.02 <= ts <= t1 + 0.02):
+                    continue
+                sm.append(float(f[1]))
+                smax = float(f[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, f[3:7]):
+            for nm, val in zip(names, f[4:8]):
                 if val.lower() == "active":
                     reasons.add(nm)
         sm.sort()
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm),
+                "samples_total": n_all}
 
 
 # ------------------------------------------------------------------- our arm
@@ -199,20 +207,22 @@ def run_ours(args):
     inr.inr_profile_enable(1)
     clocks = Clocks(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.5)   # nvidia-smi start-up: its first samples land before the timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record()
+    t_host0 = time.time()
     d.fit(vol, args.steps, B_U, opts, stream, report=False)
     ev1.record()
     torch.cuda.synchronize()
+    t_host1 = time.time()
     if world > 1:
         dist.barrier()
     ms_outer = ev0.elapsed_time(ev1)            # includes the host-side graph capture of the K steps
     ms = inr.inr_profile_span()                 # device time: first kernel start -> last kernel end
-    clk = clocks.stop()
+    clk = clocks.stop(t_host0, t_host1)
     launches = inr.inr_kernel_launches() - launches0
     prof = {k: inr.inr_profile_read(k)
             for k in ("step_begin", "sample", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "fit_fp32", "adam")}
