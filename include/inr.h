@@ -205,10 +205,14 @@ INR_API inr_status inr_value_range(const inr_view* view, float* minmax_dev, cuda
 
 /* ---- the temporal window ---- */
 typedef struct inr_cache inr_cache;
-/* capacity >= 1 timesteps; host_resident != 0 keeps snapshots in pinned host
- * memory ("cached in system RAM") and stages them to the device on
- * decode; otherwise snapshots stay in device memory. */
-INR_API inr_status cache_create(int32_t capacity, int32_t host_resident, int device, inr_cache** out);
+/* capacity >= 1 timesteps; flags (bitmask): CACHE_HOST_RESIDENT keeps snapshots in
+ * pinned host memory ("cached in system RAM") and stages them to the device
+ * on decode; CACHE_FP16 stores the parameters as fp16 (half the bytes, 2x the
+ * compression ratio; decode widens them back to fp32 — SURVEY §8(f) NEXT-4).
+ * Otherwise snapshots stay fp32 in device memory.  Staged copies live until the
+ * slot is evicted. */
+enum { CACHE_HOST_RESIDENT = 1, CACHE_FP16 = 2 };
+INR_API inr_status cache_create(int32_t capacity, int32_t flags, int device, inr_cache** out);
 INR_API inr_status cache_destroy(inr_cache* c);
 /* Copy a frozen parameter snapshot (no optimizer state) of `nblocks`
  * models as timestep `timestep` (> every cached timestep); when full,

@@ -180,7 +180,8 @@ struct inr_model {
   bool frozen = false;       // cache snapshot: parameters only
   bool host_resident = false;
   float* host_params = nullptr;  // pinned copy (host-resident snapshot)
-  bool staged = false;           // params (device) holds the host copy
+  bool staged = false;           // params (device) holds the host / fp16 copy
+  __half* h16 = nullptr;         // fp16-stored snapshot (device, or pinned host if host_resident)
 };
 
 static inr_status validate_config(const inr_config* c) {
@@ -361,9 +362,10 @@ extern "C" inr_status inr_reset(inr_model* m, uint64_t seed) {
 extern "C" inr_status inr_destroy(inr_model* m) {
   if (!m) return INR_OK;
   cudaSetDevice(m->device);
-  if (m->host_resident && m->params) cudaFree(m->params);
+  if ((m->host_resident || m->h16) && m->params) cudaFree(m->params);
   if (m->mem) cudaFree(m->mem);
   if (m->host_params) cudaFreeHost(m->host_params);
+  if (m->h16) { if (m->host_resident) cudaFreeHost(m->h16); else cudaFree(m->h16); }
   delete m;
   return INR_OK;
 }
@@ -405,9 +407,22 @@ extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
 // Make sure device-resident parameters exist for a (possibly host-resident) model.
 static inr_status ensure_device_params(const inr_model* cm, cudaStream_t st) {
   inr_model* m = const_cast<inr_model*>(cm);
-  if (!m->host_resident || m->staged) return INR_OK;
+  if (m->staged || (!m->host_resident && !m->h16)) return INR_OK;
   if (!m->params) CK(cudaMalloc((void**)&m->params, (size_t)m->P_pad * 4));
-  CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P_pad * 4, cudaMemcpyHostToDevice, st));
+  if (m->h16) {   // fp16-stored snapshot: widen into the fp32 staging buffer
+    const __half* src = m->h16;
+    void* tmp = nullptr;
+    if (m->host_resident) {
+      CK(cudaMallocAsync(&tmp, (size_t)m->P_pad * 2, st));
+      CK(cudaMemcpyAsync(tmp, m->h16, (size_t)m->P_pad * 2, cudaMemcpyHostToDevice, st));
+      src = (const __half*)tmp;
+    }
+    launch_convert_f16_f32(src, m->params, m->P_pad, st);
+    CK_LAUNCH("convert_f16_f32");
+    if (tmp) CK(cudaFreeAsync(tmp, st));
+  } else {
+    CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P_pad * 4, cudaMemcpyHostToDevice, st));
+  }
   m->staged = true;
   return INR_OK;
 }
@@ -807,6 +822,11 @@ static inr_status copy_out(const inr_model* m, const float* src, float* host, in
 }
 
 extern "C" inr_status inr_get_params(const inr_model* m, float* host, int64_t n) {
+  if (m && m->h16 && !m->staged) {
+    CK(cudaSetDevice(m->device));
+    inr_status s = ensure_device_params(m, 0);
+    if (s) return s;
+  }
   if (m && m->host_resident && !m->staged) {
     if (!host || n != m->P) return fail(INR_ERR_INVALID_ARG, "bad arguments");
     return copy_tensors(m->net, host, m->host_params, cudaMemcpyHostToHost);
@@ -864,6 +884,7 @@ struct CacheSlot {
 struct inr_cache {
   int capacity;
   bool host_resident;
+  bool fp16;
   int device;
   std::deque<CacheSlot> slots;
   int64_t bytes = 0;
@@ -871,13 +892,13 @@ struct inr_cache {
 
 static void free_slot(inr_cache* c, CacheSlot& s) {
   for (inr_model* m : s.models) {
-    c->bytes -= m->P * 4;
+    c->bytes -= m->P * (c->fp16 ? 2 : 4);
     inr_destroy(m);
   }
   s.models.clear();
 }
 
-extern "C" inr_status cache_create(int32_t capacity, int32_t host_resident, int device, inr_cache** out) {
+extern "C" inr_status cache_create(int32_t capacity, int32_t flags, int device, inr_cache** out) {
   if (!out) return fail(INR_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (capacity < 1) return fail(INR_ERR_INVALID_ARG, "capacity must be >= 1");
@@ -886,7 +907,9 @@ extern "C" inr_status cache_create(int32_t capacity, int32_t host_resident, int 
   if (device < 0 || device >= ndev) return fail(INR_ERR_INVALID_ARG, "device %d out of range", device);
   inr_cache* c = new inr_cache();
   c->capacity = capacity;
-  c->host_resident = host_resident != 0;
+  if (flags & ~(CACHE_HOST_RESIDENT | CACHE_FP16)) { delete c; return fail(INR_ERR_INVALID_ARG, "unknown cache flags"); }
+  c->host_resident = (flags & CACHE_HOST_RESIDENT) != 0;
+  c->fp16 = (flags & CACHE_FP16) != 0;
   c->device = device;
   *out = c;
   return INR_OK;
@@ -942,20 +965,42 @@ extern "C" inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* co
     m->vmax = src->vmax;
     m->steps = src->steps;
     m->frozen = true;
-    inr_status s = alloc_model(m, true, c->host_resident);
+    inr_status s = alloc_model(m, true, c->host_resident || c->fp16);
     if (s) { delete m; for (auto* x : slot.models) inr_destroy(x); return s; }
-    if (c->host_resident) {
+    m->host_resident = c->host_resident;
+    m->staged = false;
+    cudaError_t e = cudaSuccess;
+    if (c->fp16) {
+      // fp16 storage (2x compression ratio, NEXT-4): narrow on the device, then keep it there or in RAM
+      void* dst = nullptr;
+      if (c->host_resident) {
+        e = cudaMallocHost(&dst, (size_t)m->P_pad * 2);
+        m->h16 = (__half*)dst;
+        void* tmp = nullptr;
+        if (e == cudaSuccess) e = cudaMallocAsync(&tmp, (size_t)m->P_pad * 2, st);
+        if (e == cudaSuccess) {
+          launch_convert_f32_f16(src->params, (__half*)tmp, m->P_pad, st);
+          e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(m->h16, tmp, (size_t)m->P_pad * 2, cudaMemcpyDeviceToHost, st);
+        if (tmp) cudaFreeAsync(tmp, st);
+      } else {
+        e = cudaMalloc(&dst, (size_t)m->P_pad * 2);
+        m->h16 = (__half*)dst;
+        if (e == cudaSuccess) {
+          launch_convert_f32_f16(src->params, m->h16, m->P_pad, st);
+          e = cudaGetLastError();
+        }
+      }
+    } else if (c->host_resident) {
       // "the learned neural network parameters are cached in system RAM"
-      cudaError_t e = cudaMallocHost((void**)&m->host_params, (size_t)m->P_pad * 4);
+      e = cudaMallocHost((void**)&m->host_params, (size_t)m->P_pad * 4);
       if (e == cudaSuccess) e = cudaMemcpyAsync(m->host_params, src->params, (size_t)m->P_pad * 4, cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2H"); }
-      m->host_resident = true;
-      m->staged = false;
     } else {
-      cudaError_t e = cudaMemcpyAsync(m->params, src->params, (size_t)m->P_pad * 4, cudaMemcpyDeviceToDevice, st);
-      if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache D2D"); }
+      e = cudaMemcpyAsync(m->params, src->params, (size_t)m->P_pad * 4, cudaMemcpyDeviceToDevice, st);
     }
-    c->bytes += m->P * 4;  // stored parameter bytes (declared count)
+    if (e != cudaSuccess) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return cuda_fail(e, "cache copy"); }
+    c->bytes += m->P * (c->fp16 ? 2 : 4);  // stored parameter bytes (declared count)
     slot.models.push_back(m);
     slot.cmodels.push_back(m);
   }

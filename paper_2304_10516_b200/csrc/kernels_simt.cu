@@ -354,6 +354,16 @@ __global__ void __launch_bounds__(kTile) probe_simt_kernel(GroupArgs g) {
   if ((t & 31) == 0) atomicAdd(md.acc + 2, e);
 }
 
+// ------------------------------------------------------- fp16 cache storage
+__global__ void convert_f32_f16_kernel(const float* __restrict__ s, __half* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __float2half_rn(s[i]);
+}
+__global__ void convert_f16_f32_kernel(const __half* __restrict__ s, float* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __half2float(s[i]);
+}
+
 // ------------------------------------------------------------ value range
 __device__ __forceinline__ void atomic_min_f(float* a, float v) {
   if (v >= 0.f) atomicMin(reinterpret_cast<int*>(a), __float_as_int(v));
@@ -492,6 +502,15 @@ void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q
   unsigned grid = (unsigned)((q + kTile - 1) / kTile);
   DISPATCH_F(qa.net.F, set_smem(decode_query_simt_kernel<FF>, sm);
              decode_query_simt_kernel<FF><<<grid, kTile, sm, st>>>(qa, xyz, q, out, dflag));
+  count_launch();
+}
+
+void launch_convert_f32_f16(const float* src, __half* dst, long long n, cudaStream_t st) {
+  convert_f32_f16_kernel<<<148 * 8, 256, 0, st>>>(src, dst, n);
+  count_launch();
+}
+void launch_convert_f16_f32(const __half* src, float* dst, long long n, cudaStream_t st) {
+  convert_f16_f32_kernel<<<148 * 8, 256, 0, st>>>(src, dst, n);
   count_launch();
 }
 

@@ -50,6 +50,8 @@ void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int r
                              const long long os[3], const float* ref, double* sse, cudaStream_t st);
 void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag,
                               cudaStream_t st);
+void launch_convert_f32_f16(const float* src, __half* dst, long long n, cudaStream_t st);
+void launch_convert_f16_f32(const __half* src, float* dst, long long n, cudaStream_t st);
 void launch_range(const float* base, const int dims[3], const long long s[3], float* minmax, cudaStream_t st);
 void launch_debug_encode(const NetDesc& net, const float* P, const float* x01, long long q, uint32_t* idx,
                          float* feat, cudaStream_t st);

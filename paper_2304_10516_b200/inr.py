@@ -24,6 +24,7 @@ INR_OK, INR_ERR_INVALID_ARG, INR_ERR_DOMAIN, INR_ERR_NONFINITE = 0, 1, 2, 3
 INR_ERR_OOM, INR_ERR_CUDA, INR_ERR_STATE, INR_ERR_UNSUPPORTED = 4, 5, 6, 7
 INR_PREC_FP32, INR_PREC_FP16_MLP = 0, 1
 INR_REDUCE_ATOMIC, INR_REDUCE_DETERMINISTIC = 0, 1
+CACHE_HOST_RESIDENT, CACHE_FP16 = 1, 2
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "DOMAIN", 3: "NONFINITE", 4: "OOM", 5: "CUDA", 6: "STATE",
                 7: "UNSUPPORTED"}
 
@@ -215,9 +216,10 @@ def inr_value_range(view, minmax_ptr, stream=0):
 
 
 # ---- cache
-def cache_create(capacity, host_resident=0, device=0):
+def cache_create(capacity, flags=0, device=0):
+    """flags: CACHE_HOST_RESIDENT | CACHE_FP16 (inr.h)."""
     h = ctypes.c_void_p()
-    _check(_lib.cache_create(capacity, host_resident, device, ctypes.byref(h)))
+    _check(_lib.cache_create(capacity, flags, device, ctypes.byref(h)))
     return h
 
 

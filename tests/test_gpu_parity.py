@@ -319,24 +319,27 @@ def test_value_range_exact():
     assert mm2.tolist() == [float(vol[8:40, 4:20].min()), float(vol[8:40, 4:20].max())]
 
 
-@pytest.mark.parametrize("host", [0, 1])
-def test_cache_fifo_and_decode_from_slot(host):
+@pytest.mark.parametrize("flags", [0, inr.CACHE_HOST_RESIDENT, inr.CACHE_FP16,
+                                   inr.CACHE_HOST_RESIDENT | inr.CACHE_FP16])
+def test_cache_fifo_and_decode_from_slot(flags):
     vol = synth.g1_analytic(16).numpy()
     blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
     vt = gpu_volume(vol)
     go = inr.inr_fit_opts_default()
     go.vmin, go.vmax = float(vol.min()), float(vol.max())
     m = make_gpu_model(blk, 1, **CFG1)
-    c = inr.cache_create(3, host, 0)
+    c = inr.cache_create(3, flags, 0)
+    fp16 = bool(flags & inr.CACHE_FP16)
     snaps = {}
     for ts in (1, 2, 3, 4):
         inr.inr_reset(m, 100 + ts)
         inr.inr_fit(m, whole_view(vt), 3, 256, go, stream())
         ev = inr.cache_insert(c, ts, [m], stream())
         assert ev == (1 if ts == 4 else -1)
-        snaps[ts] = get_params(m)
+        p = get_params(m)
+        snaps[ts] = p.astype(np.float16).astype(np.float32) if fp16 else p
     assert inr.cache_size(c) == 3
-    assert inr.cache_bytes(c) == 3 * inr.inr_param_bytes(m)
+    assert inr.cache_bytes(c) == 3 * inr.inr_param_bytes(m) // (2 if fp16 else 1)
     with pytest.raises(inr.InrError):
         inr.cache_insert(c, 4, [m], stream())
     ts, blocks = inr.cache_get(c, 0)
