@@ -109,6 +109,24 @@ def run_cfg2(stream, prec):
     return r
 
 
+def run_cfg2r(stream, prec, log2t=15):
+    """NOT a BASELINE config: cfg2's data with right-sized tables (T = 2^15), to show
+    the PSNR @ ratio trade-off where the model is smaller than the data (R24)."""
+    n = 256
+    dev = torch.device("cuda")
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **dict(NET2, log2_table_size=log2t)))
+    vol = gen_local("g2", (n, n, n), d.lo, d.hi, dev)
+    d.value_range(vol, stream)
+    ms, coords, _ = fit_and_measure(d, vol, 2000, 65536, 16384, stream)
+    p, dms, nvox = psnr_1x(d, vol, stream)
+    r = {"config": f"cfg2r (not BASELINE: cfg2 with T = 2^{log2t})", "precision": "fp16" if prec else "fp32",
+         "fit_coords_per_s": coords / (ms / 1e3), "fit_ms_per_step": ms / 1998,
+         "decode_voxels_per_s": nvox / (dms / 1e3), "psnr_db": p, "steps": 2000,
+         "compression_ratio": ratio(d, n ** 3), "compression_ratio_fp16_stored": 2 * ratio(d, n ** 3)}
+    d.close()
+    return r
+
+
 def run_cfg3(stream, prec):
     """512^3 G3, 64 blocks on one GPU, cfg2 network, 1000 steps; decode 1x and 2x
     (2x against the analytic field)."""
@@ -155,14 +173,14 @@ def run_cfg3(stream, prec):
     return r
 
 
-def run_cfg4(stream, prec, timesteps=100, window=40, steps=500):
+def run_cfg4(stream, prec, timesteps=100, window=40, steps=500, cache_flags=inr.CACHE_FP16):
     """Temporal cache: per timestep of an evolving G2 256^3
     field, reset + fit 500 steps, insert into a window of 40 (FIFO evicts);
     every 10th insert decodes a random cached timestep at 256^3."""
     n = 256
     dev = torch.device("cuda")
     d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
-    cache = inr.cache_create(window, 0, 0)
+    cache = inr.cache_create(window, cache_flags, 0)
     rs = np.random.default_rng(4)
     fit_ms, psnrs, bytes_curve, trig = [], [], [], []
     opts = inr.inr_fit_opts_default()
@@ -212,7 +230,8 @@ def run_cfg4(stream, prec, timesteps=100, window=40, steps=500):
          "psnr_db_mean": float(np.mean(psnrs)), "psnr_db_min": float(np.min(psnrs)),
          "cache_bytes_final": bytes_curve[-1], "cache_bytes_max": max(bytes_curve),
          "cache_bytes_curve_every10": bytes_curve[::10], "evictions": timesteps - window,
-         "triggers": trig, "compression_ratio": ratio(d, n ** 3),
+         "triggers": trig, "compression_ratio": ratio(d, n ** 3) * (2 if cache_flags & inr.CACHE_FP16 else 1),
+         "cache_storage": "fp16" if cache_flags & inr.CACHE_FP16 else "fp32",
          "raw_bytes_window": window * 4 * n ** 3}
     inr.cache_destroy(cache)
     d.close()
@@ -264,18 +283,19 @@ def run_cfg5(stream, prec):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="cfg1,cfg2,cfg3,cfg4,cfg5")
+    ap.add_argument("--only", default="cfg1,cfg2,cfg2r,cfg3,cfg4,cfg5")
     ap.add_argument("--precision", default="fp16,fp32")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_configs.json"))
     a = ap.parse_args()
     torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
-    fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5}
+    fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg2r": run_cfg2r, "cfg3": run_cfg3, "cfg4": run_cfg4,
+           "cfg5": run_cfg5}
     results = []
     for name in a.only.split(","):
         for p in a.precision.split(","):
             prec = inr.INR_PREC_FP16_MLP if p == "fp16" else inr.INR_PREC_FP32
-            if name in ("cfg3", "cfg4", "cfg5") and p == "fp32":
+            if name in ("cfg2r", "cfg3", "cfg4", "cfg5") and p == "fp32":
                 continue          # the fp32 CUDA-core path is the parity mode; large configs run fp16
             t0 = time.time()
             r = fns[name](stream, prec)

@@ -631,8 +631,8 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
     {
       // features straight into this thread's row of the h_0 tile (no staging array)
       uint8_t* row = smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0];
-#pragma unroll 1
-      for (int l = 0; l < net.L; ++l) {
+#pragma unroll 4
+      for (int l = 0; l < net.L; ++l) {   // unrolled: several levels' gathers in flight
         float fl[F];
         if (MODE == 0) encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
         else encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
