@@ -70,8 +70,9 @@ enum { INR_REDUCE_ATOMIC = 0,          /* fp32 atomics: fastest, run-to-run roun
 
 /* Network configuration.
  *   levels L >= 1, features F in {1,2,4,8}, table size T = 2^log2_table_size
- *   (1..24), base resolution N_min >= 1, per_level_scale b > 1; level l has
- *   resolution N_l = floor(N_min * b^l) [R3] and min(T, (N_l+1)^3) entries
+ *   (1..30), base resolution N_min >= 1, per_level_scale b > 1; level l has
+ *   resolution N_l = floor(N_min * b^l) [R3], at most 2^30 (the cell index is an
+ *   int32: INR_ERR_INVALID_ARG beyond), and min(T, (N_l+1)^3) entries
  *   (dense x-fastest index when (N_l+1)^3 <= T, else the spatial hash of S:L236) [R1, R2].
  *   mlp_width W = 64 (this build), mlp_hidden_layers H in 1..8 (H hidden layers
  *   => H+1 weight matrices [R16]), out_dim D = 1, mlp_bias in {0,1} [R15].

@@ -192,6 +192,10 @@ static inr_status validate_config(const inr_config* c) {
     return fail(INR_ERR_INVALID_ARG, "log2_table_size must be in 1..30 (T a power of two)");
   if (c->base_resolution < 1) return fail(INR_ERR_INVALID_ARG, "base_resolution must be >= 1");
   if (!(c->per_level_scale > 1.f)) return fail(INR_ERR_INVALID_ARG, "per_level_scale must be > 1");
+  if (c->levels >= 1 &&
+      std::floor((double)c->base_resolution * std::pow((double)c->per_level_scale, (double)(c->levels - 1))) >
+          (double)(1 << 30))
+    return fail(INR_ERR_INVALID_ARG, "finest level resolution N_{L-1} exceeds 2^30 (int32 cell index) [R3]");
   if (c->mlp_hidden_layers < 1) return fail(INR_ERR_INVALID_ARG, "mlp_hidden_layers must be >= 1");
   if (c->mlp_width < 1) return fail(INR_ERR_INVALID_ARG, "mlp_width must be >= 1");
   if (c->out_dim < 1) return fail(INR_ERR_INVALID_ARG, "out_dim must be >= 1");

@@ -67,7 +67,8 @@ def test_argument_validation_without_device():
     assert L.inr_create(None, None, 0, ctypes.byref(h)) == inr.INR_ERR_INVALID_ARG
     assert "NULL" in inr.inr_last_error()
     blk = inr.make_block((0, 0, 0), (8, 8, 8), (8, 8, 8))
-    bad = [dict(levels=0), dict(log2_table_size=0), dict(per_level_scale=1.0), dict(mlp_hidden_layers=0)]
+    bad = [dict(levels=0), dict(log2_table_size=0), dict(per_level_scale=1.0), dict(mlp_hidden_layers=0),
+           dict(levels=32, base_resolution=4, per_level_scale=2.0)]          # N_31 = 2^33 > 2^30
     for kw in bad:
         cfg = inr.make_config(**{**dict(levels=4, log2_table_size=10), **kw})
         assert L.inr_create(ctypes.byref(cfg), ctypes.byref(blk), 0, ctypes.byref(h)) == inr.INR_ERR_INVALID_ARG

@@ -1,0 +1,96 @@
+"""Parity at BASELINE.json's full cfg2 sizes, in the launch configuration
+bench.py times ("at full sizes ... on sampled outputs the
+oracle can compute one by one"): 128^3 blocks of the 256^3 G2 volume, 16
+levels x 2 features, T = 2^19, 3 x 64 fp16 tensor-core MLP, 65536 uniform +
+16384 boundary samples per step, fp32-atomic gradient reduction.
+
+* one fit step's gradients, every entry of all 16.8 M parameters, in the
+  branch-free regime (R27) — the oracle runs the whole 81920-sample step;
+* the 128^3 grid decode and 2^16 bucketed queries over all 8 blocks, on
+  20000 sampled voxels / all queries, after 30 real fit steps."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import decode as o_decode, fit as o_fit, sampler
+from oracle.model import InrModel
+from paper_2304_10516_b200 import inr
+
+from gpu_util import gpu_volume, get_grads, get_params, make_gpu_model, normwise, oracle_config, per_tensor_rel, \
+    stream, whole_view
+from test_gpu_parity import componentwise_ratio, gradient_abs_bound, linear_regime
+
+pytestmark = pytest.mark.gpu
+
+CFG2 = dict(levels=16, features=2, log2_table_size=19, mlp_hidden_layers=3)
+SIDE, BLOCK, B_U, B_B = 256, 128, 65536, 16384
+
+
+@pytest.fixture(scope="module")
+def g2():
+    return synth.g2_energy(SIDE, device="cuda").cpu().numpy()
+
+
+@pytest.mark.parametrize("prec", [1, 0])
+def test_fullsize_step_gradients(g2, prec):
+    """fp32 (atomic reduction, as benched): per tensor <= 1e-4; fp16: componentwise within 2(H+2) u g_abs
+    (see test_gpu_parity.test_gradients_linear_regime_architectures)."""
+    blk = sampler.decompose(g2.shape[::-1], (BLOCK,) * 3)[5]          # interior block: 3 shared faces
+    cfg = oracle_config(**CFG2)
+    p0, lo, hi, om = linear_regime(cfg, blk, g2, 13, B_U, B_B, np.random.default_rng(11))
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=B_B)
+    m = make_gpu_model(blk, 13, reduction=0, precision=prec, **CFG2)
+    inr.inr_set_params(m, p0)
+    vt = gpu_volume(g2)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, B_B
+    inr.inr_fit(m, whole_view(vt), 1, B_U, go, stream())
+    o_fit.train_step(om, g2, opts, B_U)
+    g = get_grads(m)
+    if prec == 0:
+        err = per_tensor_rel(cfg, g, om.g)
+        print("fp32 full-size per-tensor grad rel err", err)
+        assert err <= 1e-4                                          # north_star, fp32 atomics as benched
+    else:
+        r = componentwise_ratio(cfg, g, om.g, gradient_abs_bound(cfg, blk, 13, p0, g2, opts, B_U)) / 2.0 ** -11
+        print("fp16 full-size componentwise err / (u g_abs)", r)
+        assert r <= 2 * (cfg.mlp_hidden_layers + 2)
+    inr.inr_destroy(m)
+
+
+def test_fullsize_decode_sampled(g2):
+    blocks = sampler.decompose(g2.shape[::-1], (BLOCK,) * 3)
+    lo, hi = float(g2.min()), float(g2.max())
+    cfg = oracle_config(**CFG2)
+    vt = gpu_volume(g2)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, B_B
+    gms, oms = [], {}
+    for b in blocks:
+        m = make_gpu_model(b, 17, precision=1, **CFG2)
+        inr.inr_fit(m, whole_view(vt), 30, B_U, go, stream())
+        gms.append(m)
+        om = InrModel(cfg, b, 17, params=get_params(m))
+        om.vmin, om.vmax = lo, hi
+        oms[b.block_id] = om
+    rng = np.random.default_rng(5)
+    # grid: block 6's 128^3 lattice at 1x resolution, 20000 sampled voxels
+    out = torch.empty((BLOCK,) * 3, device="cuda")
+    inr.inr_decode_grid(gms[6], (BLOCK,) * 3, out.data_ptr(), None, None, None, stream())
+    torch.cuda.synchronize()
+    j = rng.integers(0, BLOCK, size=(20000, 3))
+    xs = (j / np.float32(BLOCK)).astype(np.float32)                 # x_j = fl32(j / R) (R19)
+    y, _ = o_fit.forward(oms[blocks[6].block_id], xs)
+    ref = o_decode.denormalize(y[:, 0], lo, hi)
+    got = out.cpu().numpy()[j[:, 2], j[:, 1], j[:, 0]]
+    assert normwise(got, ref) <= 2e-3
+    # queries: bench's launch (all of the rank's blocks, bucketed, tensor-core MLP)
+    pts = synth.random_points(1 << 16, g2.shape[::-1])
+    pd = torch.from_numpy(pts).cuda()
+    q = torch.empty(pts.shape[0], device="cuda")
+    inr.inr_decode_group(gms, pd.data_ptr(), pts.shape[0], q.data_ptr(), 0, stream())
+    torch.cuda.synchronize()
+    assert normwise(q.cpu().numpy(), o_decode.decode_query(oms, pts)) <= 2e-3
+    for m in gms:
+        inr.inr_destroy(m)

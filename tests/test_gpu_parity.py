@@ -141,15 +141,97 @@ def test_one_step_gradients_and_adam_fp32(det, tol):
     inr.inr_destroy(m)
 
 
-def _linear_regime_params(cfg, blk, rng):
-    """O(0.1) tables and large positive biases: every ReLU is active (the MLP is
-    linear on the batch), so GPU and oracle cannot branch differently."""
-    p = _perturbed_params(cfg, blk, 1, rng)
-    for name, shape, off in cfg.tensor_layout():
-        if name.startswith("b"):
-            k = int(name[1:])
-            p[off:off + int(np.prod(shape))] = 0.0 if k == cfg.mlp_hidden_layers else 1.0 + 7.0 * k
-    return p
+def linear_regime(cfg, blk, vol, seed, batch, boundary_batch, rng):
+    """Parameters and a value range for which one fit step is branch-free on
+    both sides (R27): O(0.1) tables; biases set layer by layer to
+    max_batch |W_k h_{k-1}| + 1, so every hidden pre-activation of the step's
+    batch is >= 1 (all ReLUs active, no kink within any rounding); and
+    (vmin, vmax) placing every target at least 1 + 1% of max|y| below its
+    output (sgn(y - t) = +1).  Bias-free nets get positive tables and weights
+    instead.  Returns (params float32, vmin, vmax, oracle model)."""
+    p = _perturbed_params(cfg, blk, 1, rng).astype(np.float32)
+    om = InrModel(cfg, blk, seed, params=p)
+    x_u, x_b, _, _, _ = o_fit.step_batch(om, vol, o_fit.FitOpts(boundary_batch=boundary_batch), batch)
+    x = np.concatenate([x_u, x_b])
+    H = cfg.mlp_hidden_layers
+    if not cfg.mlp_bias:
+        for name, shape, off in cfg.tensor_layout():
+            n = int(np.prod(shape))
+            p[off:off + n] = np.abs(p[off:off + n]) + (np.float32(0.01) if name.startswith("table") else 0)
+    else:
+        for k in range(H):
+            _, cache = o_fit.forward(InrModel(cfg, blk, seed, params=p), x)
+            b = om.view(p, f"b{k}")
+            pre = cache[3][k] - b.astype(np.float64)[None, :]
+            b[...] = (np.abs(pre).max(axis=0) + 1.0).astype(np.float32)
+        om.view(p, f"b{H}")[...] = 0.0
+    om = InrModel(cfg, blk, seed, params=p)
+    y, cache = o_fit.forward(om, x)
+    assert all(float(z.min()) >= 0.5 for z in cache[3][:-1]) or not cfg.mlp_bias
+    assert all(float(z.min()) > 0 for z in cache[3][:-1])
+    lo = float(vol.max()) - float(y.min()) + 1.0 + 0.01 * float(np.abs(y).max())
+    return p, lo, lo + 1.0, om
+
+
+def gradient_abs_bound(cfg, blk, seed, p, vol, opts, batch):
+    """The oracle's gradient of the same step with every parameter replaced by
+    its absolute value (dy > 0 and all ReLUs active in the linear regime):
+    the |W_k|...|dy| products that bound a rounded evaluation componentwise,
+    |fl(g) - g| <= kappa * u * g_abs (the standard error bound of a chain of
+    matrix products, e.g. Higham, Accuracy and Stability, Sec. 3.5)."""
+    oa = InrModel(cfg, blk, seed, params=np.abs(p))
+    oa.vmin, oa.vmax = opts.vmin, opts.vmax
+    o_fit.train_step(oa, vol, opts, batch)
+    return oa.g
+
+
+def componentwise_ratio(cfg, g, g_ref, g_abs):
+    """max |g - g_ref| / g_abs over entries some sample touched (untouched
+    entries must be exactly zero on both sides)."""
+    nz = g_abs > 0
+    assert np.all(g[~nz] == 0) and np.all(g_ref[~nz] == 0)
+    return float(np.max(np.abs(g[nz] - g_ref[nz]) / g_abs[nz]))
+
+
+PAPER_NET = dict(levels=16, features=4, log2_table_size=14, mlp_hidden_layers=4)   # P:L217-218 (T scaled down)
+ARCHS = [CFG1, PAPER_NET, dict(levels=4, features=8, log2_table_size=12, mlp_hidden_layers=1),
+         dict(levels=16, features=1, log2_table_size=12, mlp_hidden_layers=3, mlp_bias=0)]
+
+
+@pytest.mark.parametrize("arch", range(len(ARCHS)))
+@pytest.mark.parametrize("prec", [0, 1])
+def test_gradients_linear_regime_architectures(arch, prec):
+    """Branch-free one-step gradient parity across encodings and MLP depths,
+    including the paper's own 16 levels x 4 features, 4 x 64 MLP.
+    fp32: per tensor <= 1e-5.  fp16 tensor-core MLP: componentwise within the
+    first-order rounding bound 2(H+2) u g_abs, u = 2^-11 (fp16 features,
+    weights, activations and dz, H+1 GEMMs each way) -- per-tensor norms are
+    no bound here, since dfeat = W0^T dz0 cancels (R27)."""
+    kw = ARCHS[arch]
+    vol = synth.g2_energy(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[6]
+    cfg = oracle_config(**kw)
+    p0, lo, hi, om = linear_regime(cfg, blk, vol, 9, 1000, 200, np.random.default_rng(7 + arch))
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=200)
+    m = make_gpu_model(blk, 9, reduction=1, precision=prec, **kw)
+    inr.inr_set_params(m, p0)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, 200
+    inr.inr_fit(m, whole_view(vt), 1, 1000, go, stream())
+    om.vmin, om.vmax = lo, hi
+    o_fit.train_step(om, vol, opts, 1000)
+    g = get_grads(m)
+    if prec == 0:
+        err = per_tensor_rel(cfg, g, om.g)
+        print(kw, "fp32 per-tensor grad rel err", err)
+        assert err <= 1e-5
+    else:
+        g_abs = gradient_abs_bound(cfg, blk, 9, p0, vol, opts, 1000)
+        r = componentwise_ratio(cfg, g, om.g, g_abs) / 2.0 ** -11
+        print(kw, "fp16 componentwise err / (u g_abs)", r, "bound", 2 * (cfg.mlp_hidden_layers + 2))
+        assert r <= 2 * (cfg.mlp_hidden_layers + 2)
+    inr.inr_destroy(m)
 
 
 @pytest.mark.parametrize("prec,tol", [(0, 1e-5), (1, 1e-2)])
@@ -161,14 +243,10 @@ def test_one_step_gradients_linear_regime(prec, tol):
     flips of samples within fp16 rounding of a kink (R27)."""
     vol = synth.g1_analytic(32).numpy()
     blk = sampler.decompose((32, 32, 32), (16, 16, 16))[3]
-    lo, hi = float(vol.max()) + 50.0, float(vol.max()) + 51.0    # t ~ -50 << y
-    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=128)
     cfg = oracle_config(**CFG1)
-    p0 = _linear_regime_params(cfg, blk, np.random.default_rng(5))
-    om = InrModel(cfg, blk, 7, params=p0)
-    x_u, x_b, _, _, _ = o_fit.step_batch(om, vol, opts, 1000)
-    _, cache = o_fit.forward(om, np.concatenate([x_u, x_b]))
-    assert min(float(z.min()) for z in cache[3][:-1]) > 0.05
+    p0, lo, hi, om = linear_regime(cfg, blk, vol, 7, 1000, 128, np.random.default_rng(5))
+    om.vmin, om.vmax = lo, hi
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=128)
     m = make_gpu_model(blk, 7, reduction=1, precision=prec, **CFG1)
     inr.inr_set_params(m, p0)
     vt = gpu_volume(vol)
