@@ -14,8 +14,15 @@ from . import fit, sampler
 
 
 def denormalize(y, vmin, vmax):
-    """v = y (vmax - vmin) + vmin (inverse of P:L173 value normalization)."""
-    return np.asarray(y, np.float64) * (float(vmax) - float(vmin)) + float(vmin)
+    """v = y (vmax - vmin) + vmin (inverse of P:L173 value normalization), per
+    channel when vmin, vmax are (D,) arrays."""
+    lo = np.asarray(vmin, np.float64)
+    return np.asarray(y, np.float64) * (np.asarray(vmax, np.float64) - lo) + lo
+
+
+def _channels(y):
+    """(n, 1) -> (n,) for scalar fields; (n, D) unchanged."""
+    return y[:, 0] if y.shape[1] == 1 else y
 
 
 def grid_coords(res):
@@ -26,13 +33,14 @@ def grid_coords(res):
 
 
 def decode_grid(model, res, chunk=1 << 16):
-    """Decoded values (R_z, R_y, R_x) float64 in data units."""
+    """Decoded values (R_z, R_y, R_x) float64 in data units, or (R_z, R_y, R_x, D)."""
     xs = grid_coords(res)
-    out = np.empty(xs.shape[0], dtype=np.float64)
+    D = model.cfg.out_dim
+    out = np.empty((xs.shape[0], D), dtype=np.float64)
     for a in range(0, xs.shape[0], chunk):
         y, _ = fit.forward(model, xs[a:a + chunk])
-        out[a:a + chunk] = denormalize(y[:, 0], model.vmin, model.vmax)
-    return out.reshape(res[2], res[1], res[0])
+        out[a:a + chunk] = denormalize(y, model.vmin, model.vmax)
+    return out.reshape(res[2], res[1], res[0]) if D == 1 else out.reshape(res[2], res[1], res[0], D)
 
 
 def route(p, n, global_dims):
@@ -57,20 +65,23 @@ def decode_query(models, p, strict=False):
     bc = route(p, n, gd)
     g = (gd + n - 1) // n
     bid = (bc[:, 2] * g[1] + bc[:, 1]) * g[0] + bc[:, 0]
-    out = np.full(p.shape[0], np.nan)
+    D = any_m.cfg.out_dim
+    out = np.full((p.shape[0], D), np.nan)
     for b in np.unique(bid):
         m = models[int(b)]
         sel = bid == b
         o = m.block.origin.astype(np.float32)
         x = (p[sel] - o[None, :]) / m.block.n.astype(np.float32)[None, :]
         y, _ = fit.forward(m, x.astype(np.float32))
-        out[sel] = denormalize(y[:, 0], m.vmin, m.vmax)
-    return out
+        out[sel] = denormalize(y, m.vmin, m.vmax)
+    return _channels(out)
 
 
 def sse_normalized(pred, ref, vmin, vmax):
-    """Sum of squared errors in normalized units, sum ((pred - ref)/(vmax - vmin))^2."""
-    d = (np.asarray(pred, np.float64) - np.asarray(ref, np.float64)) / (float(vmax) - float(vmin))
+    """Sum of squared errors in normalized units, sum ((pred - ref)/(vmax - vmin))^2
+    (over voxels and channels)."""
+    d = (np.asarray(pred, np.float64) - np.asarray(ref, np.float64)) / (np.asarray(vmax, np.float64) -
+                                                                        np.asarray(vmin, np.float64))
     return float(np.sum(d * d))
 
 

@@ -88,8 +88,10 @@ def train_step(model, volume, opts, batch):
     x = np.concatenate([x_u, x_b], axis=0)
     y, cache = forward(model, x)
     nu = x_u.shape[0]
-    _, l1u, l1b, dy_u, dy_b = loss.loss_and_grad(y[:nu, 0], t_u, y[nu:, 0], t_b, opts.lam)
-    dy = np.concatenate([dy_u, dy_b])[:, None]
+    D = y.shape[1]
+    yu, yb = (y[:nu, 0], y[nu:, 0]) if D == 1 else (y[:nu], y[nu:])
+    _, l1u, l1b, dy_u, dy_b = loss.loss_and_grad(yu, t_u, yb, t_b, opts.lam)
+    dy = np.concatenate([dy_u, dy_b]).reshape(-1, D)
     model.g = gradients(model, x, dy, cache)
     adam.adam_update(model.p, model.g, model.m, model.v, s + 1, lr, opts.beta1, opts.beta2, opts.eps)
     model.step += 1
@@ -101,7 +103,7 @@ def probe_psnr(model, volume, opts):
     xp = sampler.probe_lattice(32)
     t, _ = sampler.targets(volume, model.block, xp, opts.vmin, opts.vmax)
     y, _ = forward(model, xp)
-    return sampler.psnr(y[:, 0], t)
+    return sampler.psnr(y[:, 0] if y.shape[1] == 1 else y, t)
 
 
 def fit(model, volume, steps, batch, opts):
@@ -109,7 +111,7 @@ def fit(model, volume, steps, batch, opts):
     probe PSNR reaches opts.target_psnr at a check interval."""
     if steps < 1 or batch < 1:
         raise ValueError("steps and batch must be >= 1")
-    model.vmin, model.vmax = float(opts.vmin), float(opts.vmax)
+    model.vmin, model.vmax = opts.vmin, opts.vmax
     rep = FitReport()
     for i in range(steps):
         l1u, l1b, const = train_step(model, volume, opts, batch)

@@ -2,14 +2,17 @@
 
     L_Total = (1 - lambda) L1(X_Uniform, Y_Uniform) + lambda L1(X_Bound, Y_Bound)
 
-L1 = mean absolute error per term; an empty boundary set makes the
+L1 = mean absolute error per term, pooled over samples and channels
+for vector fields (D = 3: mean over the n x D residuals, as S:L78 pools the
+MSE; R28); an empty boundary set makes the
 effective lambda' = 0 (R11); subgradient sgn(0) = 0 (R11).
 """
 import numpy as np
 
 
 def loss_and_grad(y_u, t_u, y_b, t_b, lam):
-    """Returns (total, l1_uniform, l1_boundary, dy_u, dy_b) in float64."""
+    """Returns (total, l1_uniform, l1_boundary, dy_u, dy_b) in float64; y, t of
+    shape (n,) or (n, D) (dy flattened in the same element order)."""
     y_u = np.asarray(y_u, np.float64).reshape(-1)
     t_u = np.asarray(t_u, np.float64).reshape(-1)
     y_b = np.asarray(y_b, np.float64).reshape(-1)

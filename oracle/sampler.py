@@ -97,15 +97,17 @@ def boundary_samples(seed, step, block, count):
 
 
 def trilinear(volume, r):
-    """Trilinear interpolation of volume[z, y, x] at node-unit positions r (n,3)
-    (x, y, z), with clamp-to-edge at the global faces (R5).  Float64."""
+    """Trilinear interpolation of volume[z, y, x] (scalar) or volume[z, y, x, c]
+    (D channels, interleaved) at node-unit positions r (n,3) (x, y, z), per
+    channel, with clamp-to-edge at the global faces (S:L39-47; R5).  Float64;
+    returns (n,) or (n, D)."""
     vol = np.asarray(volume)
     dims = np.array([vol.shape[2], vol.shape[1], vol.shape[0]], dtype=np.int64)
     r = np.clip(np.asarray(r, np.float64), 0.0, (dims - 1).astype(np.float64))
     i0 = np.floor(r).astype(np.int64)
     f = r - i0
     i1 = np.minimum(i0 + 1, dims - 1)
-    out = np.zeros(r.shape[0], dtype=np.float64)
+    out = np.zeros((r.shape[0],) + vol.shape[3:], dtype=np.float64)
     for c in range(8):
         b = [(c >> d) & 1 for d in range(3)]
         ix = i1[:, 0] if b[0] else i0[:, 0]
@@ -114,18 +116,24 @@ def trilinear(volume, r):
         w = np.ones(r.shape[0])
         for d in range(3):
             w = w * (f[:, d] if b[d] else 1.0 - f[:, d])
-        out += w * vol[iz, iy, ix].astype(np.float64)
+        out += w.reshape((-1,) + (1,) * (vol.ndim - 3)) * vol[iz, iy, ix].astype(np.float64)
     return out
 
 
 def normalize_values(v, vmin, vmax):
     """t = (v - vmin) / (vmax - vmin) with the shared global range (P:L205;
-    S:L66-74).  A constant field (vmax == vmin) gives t = 0.
-    Returns (t, constant_flag)."""
+    S:L66-74), per channel for vector fields (vmin, vmax of shape (D,)
+    "normalized per-channel with a shared global range per channel").  A
+    constant channel (vmax == vmin) gives t = 0.
+    Returns (t, constant_flag), the flag set when every channel is constant."""
     v = np.asarray(v, np.float64)
-    if float(vmax) == float(vmin):
-        return np.zeros_like(v), True
-    return (v - float(vmin)) / (float(vmax) - float(vmin)), False
+    lo = np.asarray(vmin, np.float64)
+    hi = np.asarray(vmax, np.float64)
+    span = hi - lo
+    const = span == 0.0
+    t = (v - lo) / np.where(const, 1.0, span)
+    t = np.where(const, 0.0, t)
+    return t, bool(np.all(const))
 
 
 def targets(volume, block, x, vmin, vmax):
@@ -138,7 +146,12 @@ def targets(volume, block, x, vmin, vmax):
 def value_range(volumes):
     """Global (vmin, vmax) over all core nodes of all partitions, as the range
     all-reduce computes it ("normalized using the same maximum and
-    minimum values"; R7)."""
+    minimum values"; R7).  Scalars for scalar fields; per-channel
+    arrays (D,) for vector fields volume[z, y, x, c]."""
+    if np.asarray(volumes[0]).ndim == 4:
+        lo = np.min([np.min(v, axis=(0, 1, 2)) for v in volumes], axis=0).astype(np.float64)
+        hi = np.max([np.max(v, axis=(0, 1, 2)) for v in volumes], axis=0).astype(np.float64)
+        return lo, hi
     lo = min(float(np.min(v)) for v in volumes)
     hi = max(float(np.max(v)) for v in volumes)
     return lo, hi

@@ -115,6 +115,29 @@ def constant_field(dims, value=0.5):
     return np.full((dims[2], dims[1], dims[0]), value, dtype=np.float32)
 
 
+def taylor_green(pos, dims, t=0.0, amp=1.0, nu=0.05, drift=0.25):
+    """G4: Taylor-Green vortex velocity (the NekRS-TGV stand-in of P:L344-346;
+    S:L509 u = sin X cos Y cos Z, v = -cos X sin Y cos Z, w = 0) on X = 2 pi
+    p / (N - 1) per axis, made time-dependent by viscous decay exp(-2 nu t) and a
+    phase drift X -> X - 2 pi drift t.  Velocity in node units per time unit
+    (amp = peak speed).  pos (..., 3) float64 torch -> (..., 3)."""
+    pos = pos.to(torch.float64)
+    dims_t = torch.tensor(dims, dtype=torch.float64, device=pos.device)
+    X = 2 * math.pi * pos / (dims_t - 1).clamp(min=1)
+    x = X[..., 0] - 2 * math.pi * drift * t
+    y, z = X[..., 1], X[..., 2]
+    a = amp * math.exp(-2.0 * nu * t)
+    u = a * torch.sin(x) * torch.cos(y) * torch.cos(z)
+    v = -a * torch.cos(x) * torch.sin(y) * torch.cos(z)
+    return torch.stack([u, v, torch.zeros_like(u)], dim=-1)
+
+
+def taylor_green_volume(n, t=0.0, amp=1.0, device="cpu", **kw):
+    """G4 on the n^3 node lattice: float32 [z, y, x, 3] (channels interleaved)."""
+    dims = (n, n, n)
+    return taylor_green(lattice(dims, device), dims, t, amp, **kw).to(torch.float32)
+
+
 def random_points(q, dims, seed=SEED):
     """q uniform global node coordinates in [0, N-1]^3, float32 (q, 3)."""
     r = np.random.default_rng(seed + 7)
