@@ -62,6 +62,8 @@ typedef enum {
 /* Thread-local text of the last non-OK status of this thread ("" if none). */
 INR_API const char* inr_last_error(void);
 
+#define INR_MAX_CHANNELS 3
+
 enum { INR_PREC_FP32 = 0,      /* MLP on CUDA cores in fp32 (parity mode) */
        INR_PREC_FP16_MLP = 1   /* MLP on tcgen05 tensor cores: fp16 operands, fp32
                                   accumulate in TMEM, fp32 master weights [R17] */ };
@@ -70,12 +72,13 @@ enum { INR_REDUCE_ATOMIC = 0,          /* fp32 atomics: fastest, run-to-run roun
 
 /* Network configuration.
  *   levels L >= 1, features F in {1,2,4,8}, table size T = 2^log2_table_size
- *   (1..30), base resolution N_min >= 1, per_level_scale b > 1; level l has
+ *   (1..24 in this build), base resolution N_min >= 1, per_level_scale b > 1; level l has
  *   resolution N_l = floor(N_min * b^l) [R3], at most 2^30 (the cell index is an
  *   int32: INR_ERR_INVALID_ARG beyond), and min(T, (N_l+1)^3) entries
  *   (dense x-fastest index when (N_l+1)^3 <= T, else the spatial hash of S:L236) [R1, R2].
  *   mlp_width W = 64 (this build), mlp_hidden_layers H in 1..8 (H hidden layers
- *   => H+1 weight matrices [R16]), out_dim D = 1, mlp_bias in {0,1} [R15].
+ *   => H+1 weight matrices [R16]), out_dim D in {1, 3} (scalar or vector field,
+ *   P:L156), mlp_bias in {0,1} [R15].
  *   L*F <= 64 and, for INR_PREC_FP16_MLP, a multiple of 16.
  *   seed selects the Philox4x32-10 streams for init (0), uniform samples (1),
  *   boundary samples (2) [R8, R14]. */
@@ -125,7 +128,10 @@ INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
  *   form [R12]; [vmin, vmax] is the global value range shared by all blocks
  *    — vmax == vmin is legal (targets 0, report.constant_field = 1);
  *   target_psnr > 0 with check_interval > 0 stops once the PSNR on a 32^3
- *   cell-centred probe lattice reaches the target. */
+ *   cell-centred probe lattice reaches the target.
+ *   Vector fields (out_dim 3) take per-channel ranges [vmin_c[c], vmax_c[c]]
+ *   instead (vmin/vmax are then ignored); the L1 terms and the probe
+ *   MSE pool over samples and channels [R28]. */
 typedef struct {
   double lambda;
   int32_t boundary_batch;
@@ -135,6 +141,7 @@ typedef struct {
   double vmin, vmax;
   double target_psnr;
   int32_t check_interval;
+  double vmin_c[INR_MAX_CHANNELS], vmax_c[INR_MAX_CHANNELS];
 } inr_fit_opts;
 INR_API void inr_fit_opts_default(inr_fit_opts* o);
 
@@ -148,12 +155,15 @@ typedef struct {
  * indices, lo[d] <= i < lo[d] + dims[d]) is base[(i-lo0)*stride0 + (j-lo1)*stride1
  * + (k-lo2)*stride2] (strides in elements).  For a block it must cover nodes
  * [o_d, min(o_d + n_d, N_d - 1)] per axis (the core plus the 1-node high-side
- * ghost layer [R6]); many blocks may share one allocation (zero-copy). */
+ * ghost layer [R6]); many blocks may share one allocation (zero-copy).
+ * channels: 0 or 1 for a scalar field; 3 for a vector field whose channel c of
+ * a node sits at +c (interleaved); it must equal the model's out_dim. */
 typedef struct {
   const float* base;
   int64_t lo[3];
   int32_t dims[3];
   int64_t stride[3];
+  int32_t channels;
 } inr_view;
 
 /* Train one model for `steps` >= 1 steps of `batch` >= 1 uniform samples plus
@@ -175,8 +185,8 @@ INR_API inr_status inr_fit_group(inr_model* const* models, const inr_view* views
                          inr_fit_report* out, cudaStream_t stream);
 
 /* Direct queries: xyz (dev) holds q global node
- * coordinates (x,y,z interleaved); out (dev) receives q values in data units
- * v = Phi(x) (vmax - vmin) + vmin.  A query p goes to the block
+ * coordinates (x,y,z interleaved); out (dev) receives q x D values in data units
+ * v = Phi(x) (vmax - vmin) + vmin (per channel, channels interleaved).  A query p goes to the block
  * min(max(floor(p/n), 0), B-1) per axis and x = fl32(fl32(p - o)/n) [R5];
  * inr_decode uses the one model, inr_decode_group routes among `nmodels`
  * models (a point whose block is not among them gets NaN).  strict != 0
@@ -189,10 +199,11 @@ INR_API inr_status inr_decode_group(const inr_model* const* models, int32_t nmod
 
 /* Decode to grid: res[d] >= 1 samples per axis at
  * x_j = fl32(j / res_d), j < res_d (half-open, so blocks tile without
- * duplicates [R19]); value written to out[jx*os0 + jy*os1 + jz*os2] where
- * os = out_stride (elements) or, if out_stride is NULL, the dense x-fastest
- * strides (1, res0, res0*res1).  If ref (dev, same layout) is non-NULL, the
- * sum over the lattice of ((pred - ref)/(vmax - vmin))^2 is atomically added
+ * duplicates [R19]); value written to out[jx*os0 + jy*os1 + jz*os2 (+ c for
+ * channel c of a vector field)] where os = out_stride (elements) or, if
+ * out_stride is NULL, the dense x-fastest strides (D, D res0, D res0 res1).
+ * If ref (dev, same layout) is non-NULL, the sum over the lattice (and
+ * channels) of ((pred - ref)/(vmax - vmin))^2 is atomically added
  * to *sse_dev (dev double; caller zeroes it; many blocks may accumulate into
  * one scalar) (S:L75-83 PSNR in normalized units [R18]).  Asynchronous. */
 INR_API inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
@@ -200,8 +211,9 @@ INR_API inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], flo
                            cudaStream_t stream);
 
 /* Min/max over the nodes of a view: atomically
- * folds into minmax_dev[0] (min) and minmax_dev[1] (max) (dev floats, caller
- * initialises to +inf/-inf).  The cross-GPU all-reduce is the caller's. */
+ * folds into minmax_dev[2c] (min) and minmax_dev[2c+1] (max) of every channel c
+ * of the view (dev floats, caller initialises to +inf/-inf).  The cross-GPU
+ * all-reduce is the caller's. */
 INR_API inr_status inr_value_range(const inr_view* view, float* minmax_dev, cudaStream_t stream);
 
 /* ---- the temporal window ---- */
@@ -244,7 +256,7 @@ INR_API inr_status inr_get_adam_state(const inr_model* m, float* m_host, float* 
 INR_API inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_t q, uint32_t* idx, float* feat,
                             cudaStream_t stream);
 /* Network output Phi(x) in normalized units for q block-normalized coordinates
- * (dev q x 3 -> dev q), in the model's configured precision.  Asynchronous. */
+ * (dev q x 3 -> dev q x D), in the model's configured precision.  Asynchronous. */
 INR_API inr_status inr_debug_forward(const inr_model* m, const float* x01, int64_t q, float* y, cudaStream_t stream);
 /* Kernel timing for benchmarks: while enabled, every kernel the library
  * launches is bracketed by CUDA events recorded on its launching stream (and

@@ -80,8 +80,10 @@ def decode_query(models, p, strict=False):
 def sse_normalized(pred, ref, vmin, vmax):
     """Sum of squared errors in normalized units, sum ((pred - ref)/(vmax - vmin))^2
     (over voxels and channels)."""
-    d = (np.asarray(pred, np.float64) - np.asarray(ref, np.float64)) / (np.asarray(vmax, np.float64) -
-                                                                        np.asarray(vmin, np.float64))
+    span = np.asarray(vmax, np.float64) - np.asarray(vmin, np.float64)
+    # a constant channel is 0 in normalized units on both sides (S:L70)
+    d = np.where(span > 0, (np.asarray(pred, np.float64) - np.asarray(ref, np.float64)) / np.where(span > 0, span, 1.0),
+                 0.0)
     return float(np.sum(d * d))
 
 

@@ -19,6 +19,7 @@ constexpr int kWidth = 64;        // MLP width of this build
 constexpr int kMaxLevels = 32;
 constexpr int kMaxLayers = 9;     // H <= 8 hidden layers => <= 9 weight matrices
 constexpr int kMaxGroup = 64;     // models per fused launch
+constexpr int kMaxD = 3;          // output channels: scalar (1) or vector (3) fields
 constexpr uint32_t kPrimeY = 2654435761u;
 constexpr uint32_t kPrimeZ = 805459861u;
 constexpr int kFixedShift = 40;   // deterministic mode: int64 fixed point with 2^-40 resolution [R21]
@@ -71,7 +72,7 @@ struct ModelDev {
   uint32_t block_id;
   int nfaces;
   int faces[6];
-  float vmin, vrange, inv_range;    // normalization (inv_range = 0 for a constant field)
+  float vmin[kMaxD], vrange[kMaxD], inv_range[kMaxD];   // per-channel normalization (inv_range 0: constant)
   uint32_t k0, k1u, k1b;            // Philox keys (seed_lo, seed_hi ^ 1), (seed_lo, seed_hi ^ 2) [R8]
 };
 
@@ -113,8 +114,10 @@ __device__ __forceinline__ void draw_sample(const ModelDev& md, int i, int B_u, 
 }
 
 // Trilinear interpolation of the view at r = o + x n (node units), clamp-to-edge,
-// then normalization with the global range.
-__device__ __forceinline__ float sample_target(const ModelDev& md, const float x[3]) {
+// then normalization with the global range, per channel for
+// vector fields (channel c of a node at +c).
+template <int D>
+__device__ __forceinline__ void sample_target(const ModelDev& md, const float x[3], float t[D]) {
   int i0[3], i1[3];
   float f[3];
 #pragma unroll
@@ -128,18 +131,22 @@ __device__ __forceinline__ float sample_target(const ModelDev& md, const float x
     // the view may end at node o + n (its contract), so node o + n + 1 must not be read
     i1[d] = f[d] > 0.f ? min(i0[d] + 1, md.N[d] - 1) : i0[d];
   }
-  float acc = 0.f;
+  float acc[D];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    int ix = (c & 1) ? i1[0] : i0[0];
-    int iy = (c & 2) ? i1[1] : i0[1];
-    int iz = (c & 4) ? i1[2] : i0[2];
-    float w = ((c & 1) ? f[0] : 1.f - f[0]) * ((c & 2) ? f[1] : 1.f - f[1]) * ((c & 4) ? f[2] : 1.f - f[2]);
+  for (int c = 0; c < D; ++c) acc[c] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int ix = (k & 1) ? i1[0] : i0[0];
+    int iy = (k & 2) ? i1[1] : i0[1];
+    int iz = (k & 4) ? i1[2] : i0[2];
+    float w = ((k & 1) ? f[0] : 1.f - f[0]) * ((k & 2) ? f[1] : 1.f - f[1]) * ((k & 4) ? f[2] : 1.f - f[2]);
     long long off = (ix - md.vlo[0]) * md.vstride[0] + (iy - md.vlo[1]) * md.vstride[1] +
                     (iz - md.vlo[2]) * md.vstride[2];
-    acc = fmaf(w, __ldg(md.vbase + off), acc);
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = fmaf(w, __ldg(md.vbase + off + c), acc[c]);
   }
-  return (acc - md.vmin) * md.inv_range;
+#pragma unroll
+  for (int c = 0; c < D; ++c) t[c] = (acc[c] - md.vmin[c]) * md.inv_range[c];
 }
 
 // ------------------------------------------------------------- level lookup

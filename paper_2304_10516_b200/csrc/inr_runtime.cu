@@ -176,7 +176,7 @@ struct inr_model {
   uint32_t block_id = 0;
   int nfaces = 0;
   int faces[6] = {0, 0, 0, 0, 0, 0};
-  float vmin = 0.f, vmax = 1.f;
+  float vmin[kMaxD] = {0.f, 0.f, 0.f}, vmax[kMaxD] = {1.f, 1.f, 1.f};   // per-channel range of the last fit
   bool frozen = false;       // cache snapshot: parameters only
   bool host_resident = false;
   float* host_params = nullptr;  // pinned copy (host-resident snapshot)
@@ -210,7 +210,7 @@ static inr_status validate_config(const inr_config* c) {
   if (c->log2_table_size > 24) return fail(INR_ERR_UNSUPPORTED, "log2_table_size must be <= 24 in this build");
   if (c->mlp_width != kWidth) return fail(INR_ERR_UNSUPPORTED, "mlp_width must be 64 in this build");
   if (c->mlp_hidden_layers > kMaxLayers - 1) return fail(INR_ERR_UNSUPPORTED, "at most 8 hidden layers");
-  if (c->out_dim != 1) return fail(INR_ERR_UNSUPPORTED, "out_dim must be 1 in this build");
+  if (c->out_dim != 1 && c->out_dim != 3) return fail(INR_ERR_UNSUPPORTED, "out_dim must be 1 or 3 in this build");
   if (c->precision == INR_PREC_FP16_MLP && (c->levels * c->features) % 16 != 0)
     return fail(INR_ERR_UNSUPPORTED, "fp16 MLP needs levels*features to be a multiple of 16");
   return INR_OK;
@@ -404,6 +404,7 @@ extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
   o->eps = 1e-8;
   o->vmin = 0.0;
   o->vmax = 1.0;
+  for (int c = 0; c < INR_MAX_CHANNELS; ++c) { o->vmin_c[c] = 0.0; o->vmax_c[c] = 1.0; }
   o->target_psnr = 0.0;
   o->check_interval = 0;
 }
@@ -451,9 +452,11 @@ static ModelDev model_dev(const inr_model* m) {
   d.block_id = m->block_id;
   d.nfaces = m->nfaces;
   for (int k = 0; k < 6; ++k) d.faces[k] = m->faces[k];
-  d.vmin = m->vmin;
-  d.vrange = m->vmax - m->vmin;
-  d.inv_range = m->vmax > m->vmin ? (float)(1.0 / ((double)m->vmax - (double)m->vmin)) : 0.f;
+  for (int c = 0; c < kMaxD; ++c) {
+    d.vmin[c] = m->vmin[c];
+    d.vrange[c] = m->vmax[c] - m->vmin[c];
+    d.inv_range[c] = m->vmax[c] > m->vmin[c] ? (float)(1.0 / ((double)m->vmax[c] - (double)m->vmin[c])) : 0.f;
+  }
   return d;
 }
 
@@ -498,7 +501,17 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   if (!(opts->lambda >= 0.0 && opts->lambda <= 1.0)) return fail(INR_ERR_INVALID_ARG, "lambda must be in [0,1]");
   if (opts->boundary_batch < 0) return fail(INR_ERR_INVALID_ARG, "boundary_batch must be >= 0");
   if (opts->lr_step < 1) return fail(INR_ERR_INVALID_ARG, "lr_step must be >= 1");
-  if (!(opts->vmax >= opts->vmin)) return fail(INR_ERR_INVALID_ARG, "vmax < vmin");
+  if (!models || !models[0]) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
+  const int D = models[0]->net.D;
+  // the per-channel ranges of this call: vmin/vmax for scalar fields, vmin_c/vmax_c for vector fields
+  double lo[kMaxD], hi[kMaxD];
+  for (int c = 0; c < D; ++c) {
+    lo[c] = D == 1 ? opts->vmin : opts->vmin_c[c];
+    hi[c] = D == 1 ? opts->vmax : opts->vmax_c[c];
+    if (!(hi[c] >= lo[c])) return fail(INR_ERR_INVALID_ARG, "vmax < vmin (channel %d)", c);
+  }
+  bool all_constant = true;
+  for (int c = 0; c < D; ++c) all_constant &= hi[c] == lo[c];
   for (int i = 0; i < nmodels; ++i) {
     if (!models[i]) return fail(INR_ERR_INVALID_ARG, "model %d is NULL", i);
     if (models[i]->frozen) return fail(INR_ERR_STATE, "model %d is a frozen cache snapshot", i);
@@ -506,6 +519,8 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       return fail(INR_ERR_INVALID_ARG, "all models of a group must share device and config");
     inr_status s = validate_view(models[i], &views[i]);
     if (s) return s;
+    if (std::max(1, views[i].channels) != D)
+      return fail(INR_ERR_INVALID_ARG, "view %d has %d channels, the model outputs %d", i, views[i].channels, D);
   }
   const inr_model* m0 = models[0];
   CK(cudaSetDevice(m0->device));
@@ -530,10 +545,11 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   as.ob2 = (float)(1.0 - opts->beta2);
   as.eps = (float)opts->eps;
 
-  for (int i = 0; i < nmodels; ++i) {
-    models[i]->vmin = (float)opts->vmin;
-    models[i]->vmax = (float)opts->vmax;
-  }
+  for (int i = 0; i < nmodels; ++i)
+    for (int c = 0; c < D; ++c) {
+      models[i]->vmin[c] = (float)lo[c];
+      models[i]->vmax[c] = (float)hi[c];
+    }
   const int nchunks = (nmodels + kMaxGroup - 1) / kMaxGroup;
   std::vector<GroupArgs> groups(nchunks);
   for (int c = 0; c < nchunks; ++c) {
@@ -571,7 +587,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
         { ProfScope p(PK_SAMPLE, s); launch_sample(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
-        { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.dfeat, ws.Bs, s); }
+        { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.targets, ws.dfeat, ws.Bs, s); }
         { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
       } else {
@@ -631,7 +647,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       for (int i = 0; i < nmodels; ++i) {
         double sse = 0;
         CK(cudaMemcpy(&sse, models[i]->acc + 2, sizeof sse, cudaMemcpyDeviceToHost));
-        double mse = sse / 32768.0;
+        double mse = sse / (32768.0 * D);
         psnr[i] = mse <= 0 ? 200.0 : std::min(200.0, -10.0 * std::log10(mse));
         reached[i] = psnr[i] >= opts->target_psnr;
         reached_all &= reached[i] != 0;
@@ -656,15 +672,15 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     inr_fit_report& r = out[i];
     r.steps_taken = taken;
     r.reached_target = reached[i];
-    r.constant_field = opts->vmax == opts->vmin;
+    r.constant_field = all_constant;
     int bb = m->nfaces > 0 ? opts->boundary_batch : 0;
-    r.loss_uniform = acc[0] / (double)batch;
-    r.loss_boundary = bb > 0 ? acc[1] / (double)bb : 0.0;
+    r.loss_uniform = acc[0] / ((double)batch * D);
+    r.loss_boundary = bb > 0 ? acc[1] / ((double)bb * D) : 0.0;
     r.probe_psnr = psnr[i];
     if (flag || !std::isfinite(r.loss_uniform) || !std::isfinite(r.loss_boundary)) nonfinite = true;
   }
   if (nonfinite) return fail(INR_ERR_NONFINITE, "non-finite loss or parameter after %d steps", taken);
-  if (opts->vmax == opts->vmin) g_err = "warning: constant field (vmax == vmin), targets are 0";
+  if (all_constant) g_err = "warning: constant field (vmax == vmin), targets are 0";
   return INR_OK;
 }
 
@@ -693,7 +709,10 @@ extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], 
   if (s) return s;
   long long os[3];
   if (out_stride) { for (int d = 0; d < 3; ++d) os[d] = out_stride[d]; }
-  else { os[0] = 1; os[1] = res[0]; os[2] = (long long)res[0] * res[1]; }
+  else {
+    const long long D = m->net.D;
+    os[0] = D; os[1] = D * res[0]; os[2] = D * res[0] * res[1];
+  }
   int r[3] = {res[0], res[1], res[2]};
   ModelDev md = model_dev(m);
   {
@@ -797,7 +816,9 @@ extern "C" inr_status inr_value_range(const inr_view* v, float* minmax, cudaStre
     if (v->dims[d] < 1) return fail(INR_ERR_INVALID_ARG, "view dims must be >= 1");
   int dims[3] = {v->dims[0], v->dims[1], v->dims[2]};
   long long s[3] = {v->stride[0], v->stride[1], v->stride[2]};
-  { ProfScope p(PK_RANGE, st); launch_range(v->base, dims, s, minmax, st); }
+  const int ch = std::max(1, v->channels);
+  if (ch != 1 && ch != 3) return fail(INR_ERR_INVALID_ARG, "view channels must be 1 or 3");
+  { ProfScope p(PK_RANGE, st); launch_range(v->base, dims, s, ch, minmax, st); }
   CK_LAUNCH("value_range");
   return INR_OK;
 }
@@ -965,8 +986,8 @@ extern "C" inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* co
     m->block_id = src->block_id;
     m->nfaces = src->nfaces;
     memcpy(m->faces, src->faces, sizeof m->faces);
-    m->vmin = src->vmin;
-    m->vmax = src->vmax;
+    memcpy(m->vmin, src->vmin, sizeof m->vmin);
+    memcpy(m->vmax, src->vmax, sizeof m->vmax);
     m->steps = src->steps;
     m->frozen = true;
     inr_status s = alloc_model(m, true, c->host_resident || c->fp16);

@@ -22,17 +22,21 @@ constexpr int kLmThreads = 256;
 constexpr int kSmemAccFloats = 12288;   // levels with S_l * F <= this accumulate in smem (48 KB)
 constexpr int kBwdChunk = 2048;         // samples per CTA in the backward scatter
 
+// samples[i] = (x, y, z, t_0); vector fields also write targets[i] = (t_0, t_1, t_2, 0).
+template <int D>
 __global__ void __launch_bounds__(kLmThreads) sample_kernel(GroupArgs g, FitScalars fs, float4* __restrict__ samples,
-                                                             int Bs) {
+                                                             float4* __restrict__ targets, int Bs) {
   const int m = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
   const int i = blockIdx.x * kLmThreads + threadIdx.x;
   if (i >= total) return;
   const uint32_t step = (uint32_t)*md.step_cur;
-  float x[3];
+  float x[3], t[D];
   draw_sample(md, i, fs.B_u, step, x);
-  samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], sample_target(md, x));
+  sample_target<D>(md, x, t);
+  samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], t[0]);
+  if constexpr (D == 3) targets[(size_t)m * Bs + i] = make_float4(t[0], t[1], t[2], 0.f);
 }
 
 // Writes straight into the tensor-core MLP's h_0 tile images (canonical layout,
@@ -266,8 +270,8 @@ size_t lm_workspace_bytes(const NetDesc& net, int nmodels, int Bs) {
   uint32_t img = 0;
   tc_fit_geometry(net, &geom, &img);
   size_t s = (size_t)nmodels * Bs;
-  return s * sizeof(float4) + (size_t)nmodels * (Bs / 128) * geom.tile_bytes + s * net.LF * sizeof(float) +
-         (size_t)nmodels * img + 4 * 256;
+  return s * sizeof(float4) * (net.D > 1 ? 2 : 1) + (size_t)nmodels * (Bs / 128) * geom.tile_bytes +
+         s * net.LF * sizeof(float) + (size_t)nmodels * img + 5 * 256;
 }
 
 LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs) {
@@ -283,13 +287,16 @@ LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs) {
   w.dfeat = reinterpret_cast<float*>(p);
   p += align(s * net.LF * sizeof(float));
   w.wimg = reinterpret_cast<uint8_t*>(p);
+  p += align((size_t)nmodels * w.img_bytes);
+  w.targets = net.D > 1 ? reinterpret_cast<float4*>(p) : nullptr;
   w.Bs = Bs;
   return w;
 }
 
 void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st) {
   dim3 grid((fs.B_u + fs.B_b + kLmThreads - 1) / kLmThreads, nmodels);
-  sample_kernel<<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.Bs);
+  if (g.net.D == 1) sample_kernel<1><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.targets, w.Bs);
+  else sample_kernel<3><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.targets, w.Bs);
   count_launch();
 }
 

@@ -66,8 +66,9 @@ __global__ void step_begin_kernel(GroupArgs g, long long zero_from) {
 // ------------------------------------------------------------ SIMT MLP fwd
 // act: smem rows of kLd floats; rows [0, LF) hold the features of the tile;
 // rows LF + 64 k + n hold the pre-activation z_k[n] of hidden layer k.
-// Returns y (D = 1).  h_{k+1} = max(z_k, 0).
-__device__ float mlp_forward_simt(const NetDesc& net, const float* __restrict__ P, float* act, int t) {
+// Writes y[0..D).  h_{k+1} = max(z_k, 0).
+__device__ void mlp_forward_simt(const NetDesc& net, const float* __restrict__ P, float* act, int t,
+                                 float y[kMaxD]) {
   const float* hin = act;
   int in = net.LF;
   bool relu = false;
@@ -88,14 +89,21 @@ __device__ float mlp_forward_simt(const NetDesc& net, const float* __restrict__ 
     in = kWidth;
     relu = true;
   }
-  const float* W = P + net.w_off[net.H];
-  float acc = net.bias ? __ldg(P + net.b_off[net.H]) : 0.f;
-  for (int i = 0; i < in; ++i) {
-    float h = hin[i * kLd + t];
-    if (relu) h = fmaxf(h, 0.f);
-    acc = fmaf(__ldg(W + i), h, acc);
+  for (int c = 0; c < net.D; ++c) {
+    const float* W = P + net.w_off[net.H] + (size_t)c * in;
+    float acc = net.bias ? __ldg(P + net.b_off[net.H] + c) : 0.f;
+    for (int i = 0; i < in; ++i) {
+      float h = hin[i * kLd + t];
+      if (relu) h = fmaxf(h, 0.f);
+      acc = fmaf(__ldg(W + i), h, acc);
+    }
+    y[c] = acc;
   }
-  return acc;
+}
+
+__device__ __forceinline__ void sample_target_rt(const ModelDev& md, int D, const float x[3], float t[kMaxD]) {
+  if (D == 1) sample_target<1>(md, x, t);
+  else sample_target<3>(md, x, t);
 }
 
 template <int F>
@@ -141,43 +149,53 @@ __global__ void __launch_bounds__(kTile) fit_simt_kernel(GroupArgs g, FitScalars
   __shared__ double red[2][kTile / 32];
 
   const uint32_t step = (uint32_t)*md.step_cur;
+  const int D = net.D;
   float x[3] = {0.f, 0.f, 0.f};
-  float target = 0.f;
+  float target[kMaxD] = {0.f, 0.f, 0.f};
   if (valid) {
     draw_sample(md, i, fs.B_u, step, x);
-    target = sample_target(md, x);
+    sample_target_rt(md, D, x, target);
   }
   encode_to_smem<F>(net, P, x, act, t);
   // No barrier needed: every thread only touches its own smem column until the
   // per-tile weight-gradient reduction below.
-  float y = mlp_forward_simt(net, P, act, t);
+  float y[kMaxD];
+  mlp_forward_simt(net, P, act, t, y);
 
-  // Eq. 2: dL/dy = (1 - lambda') sgn(y - t) / B_u  (uniform)  or  lambda' sgn / B_b.
+  // Eq. 2 (L1 pooled over the D channels, R28): dL/dy_c = (1 - lambda') sgn(y_c - t_c) / (B_u D)
+  // (uniform) or lambda' sgn / (B_b D).
   float lam = B_b > 0 ? fs.lambda : 0.f;
   bool is_b = i >= fs.B_u;
-  float d = y - target;
-  float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
-  float dy = is_b ? lam * sg / (float)max(B_b, 1) : (1.f - lam) * sg / (float)fs.B_u;
+  float dy[kMaxD];
+  double ad = 0.0;
+  for (int c = 0; c < D; ++c) {
+    float d = y[c] - target[c];
+    float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
+    dy[c] = is_b ? lam * sg / (float)(max(B_b, 1) * D) : (1.f - lam) * sg / (float)(fs.B_u * D);
+    ad += fabs((double)d);
+  }
   {
-    double au = (valid && !is_b) ? fabs((double)d) : 0.0;
-    double ab = (valid && is_b) ? fabs((double)d) : 0.0;
+    double au = (valid && !is_b) ? ad : 0.0;
+    double ab = (valid && is_b) ? ad : 0.0;
     au = warp_sum(au);
     ab = warp_sum(ab);
     if ((t & 31) == 0) { red[0][t >> 5] = au; red[1][t >> 5] = ab; }
   }
 
-  // ---- backward through the output layer (D = 1)
+  // ---- backward through the output layer
   const int H = net.H;
   const float* hH = act + (size_t)(net.LF + kWidth * (H - 1)) * kLd;   // z_{H-1}
   {
     const float* Wo = P + net.w_off[H];
     for (int n = 0; n < kWidth; ++n) {
       float z = hH[n * kLd + t];
-      dzA[n * kLd + t] = z > 0.f ? __ldg(Wo + n) * dy : 0.f;          // dz_{H-1}
+      float acc = 0.f;
+      for (int c = 0; c < D; ++c) acc = fmaf(__ldg(Wo + (size_t)c * kWidth + n), dy[c], acc);
+      dzA[n * kLd + t] = z > 0.f ? acc : 0.f;                            // dz_{H-1}
     }
   }
-  __shared__ float dys[kTile];
-  dys[t] = dy;
+  __shared__ float dys[kMaxD][kTile];
+  for (int c = 0; c < D; ++c) dys[c][t] = dy[c];
   __syncthreads();
   if (t == 0) {
     double su = 0, sb = 0;
@@ -185,15 +203,15 @@ __global__ void __launch_bounds__(kTile) fit_simt_kernel(GroupArgs g, FitScalars
     if (su != 0.0) atomicAdd(md.acc + 0, su);
     if (sb != 0.0) atomicAdd(md.acc + 1, sb);
   }
-  // dW_H[0][n] = sum_s dy_s relu(z_{H-1}[n][s]); db_H = sum_s dy_s  (thread n owns entry n)
-  {
+  // dW_H[c][n] = sum_s dy_c,s relu(z_{H-1}[n][s]); db_H[c] = sum_s dy_c,s  (thread n owns column n)
+  for (int c = 0; c < D; ++c) {
     float acc = 0.f;
-    for (int s = 0; s < kTile; ++s) acc = fmaf(dys[s], fmaxf(hH[t * kLd + s], 0.f), acc);
-    if (acc != 0.f) grad_add(G, GX, net.w_off[H] + t, acc);
+    for (int s = 0; s < kTile; ++s) acc = fmaf(dys[c][s], fmaxf(hH[t * kLd + s], 0.f), acc);
+    if (acc != 0.f) grad_add(G, GX, net.w_off[H] + (size_t)c * kWidth + t, acc);
     if (net.bias && t == 0) {
       float b = 0.f;
-      for (int s = 0; s < kTile; ++s) b += dys[s];
-      if (b != 0.f) grad_add(G, GX, net.b_off[H], b);
+      for (int s = 0; s < kTile; ++s) b += dys[c][s];
+      if (b != 0.f) grad_add(G, GX, net.b_off[H] + c, b);
     }
   }
   // ---- hidden layers k = H-1 .. 0:  z_k = W_k h_k + b_k
@@ -285,15 +303,19 @@ __global__ void __launch_bounds__(kTile) decode_grid_simt_kernel(NetDesc net, Mo
   }
   float x[3] = {__fdiv_rn((float)jx, (float)rx), __fdiv_rn((float)jy, (float)ry), __fdiv_rn((float)jz, (float)rz)};
   encode_to_smem<F>(net, md.params, x, smem, t);
-  float y = mlp_forward_simt(net, md.params, smem, t);
+  float y[kMaxD];
+  mlp_forward_simt(net, md.params, smem, t, y);
   double e = 0.0;
   if (valid) {
     long long off = jx * os0 + jy * os1 + jz * os2;
-    float v = fmaf(y, md.vrange, md.vmin);
-    out[off] = v;
-    if (ref) {
-      double dd = ((double)v - (double)__ldg(ref + off)) / (double)md.vrange;
-      e = dd * dd;
+    for (int c = 0; c < net.D; ++c) {
+      float v = fmaf(y[c], md.vrange[c], md.vmin[c]);
+      out[off + c] = v;
+      if (ref) {
+        // a constant channel (vrange 0) is 0 in normalized units on both sides
+        double dd = md.vrange[c] > 0.f ? ((double)v - (double)__ldg(ref + off + c)) / (double)md.vrange[c] : 0.0;
+        e += dd * dd;
+      }
     }
   }
   if (sse) {
@@ -329,9 +351,12 @@ __global__ void __launch_bounds__(kTile) decode_query_simt_kernel(QueryArgs qa, 
   float x[3];
   for (int d = 0; d < 3; ++d) x[d] = __fdiv_rn(__fsub_rn(p[d], (float)md.o[d]), (float)md.n[d]);
   encode_to_smem<F>(qa.net, md.params, x, smem, t);
-  float y = mlp_forward_simt(qa.net, md.params, smem, t);
+  float y[kMaxD];
+  mlp_forward_simt(qa.net, md.params, smem, t, y);
   if (valid) {
-    out[j] = slot < 0 ? __int_as_float(0x7fc00000) : fmaf(y, md.vrange, md.vmin);
+    const int D = qa.net.D;
+    for (int c = 0; c < D; ++c)
+      out[j * D + c] = slot < 0 ? __int_as_float(0x7fc00000) : fmaf(y[c], md.vrange[c], md.vmin[c]);
     if (outside && domain_flag) atomicOr(domain_flag, 1);
   }
 }
@@ -346,10 +371,12 @@ __global__ void __launch_bounds__(kTile) probe_simt_kernel(GroupArgs g) {
   const int t = threadIdx.x;
   const int j = blockIdx.x * kTile + t;  // < 32768
   float x[3] = {((j & 31) + 0.5f) / 32.f, (((j >> 5) & 31) + 0.5f) / 32.f, ((j >> 10) + 0.5f) / 32.f};
-  float tgt = sample_target(md, x);
+  float tgt[kMaxD], y[kMaxD];
+  sample_target_rt(md, g.net.D, x, tgt);
   encode_to_smem<F>(g.net, md.params, x, smem, t);
-  float y = mlp_forward_simt(g.net, md.params, smem, t);
-  double e = (double)(y - tgt) * (double)(y - tgt);
+  mlp_forward_simt(g.net, md.params, smem, t, y);
+  double e = 0.0;
+  for (int c = 0; c < g.net.D; ++c) e += (double)(y[c] - tgt[c]) * (double)(y[c] - tgt[c]);
   e = warp_sum(e);
   if ((t & 31) == 0) atomicAdd(md.acc + 2, e);
 }
@@ -374,8 +401,11 @@ __device__ __forceinline__ void atomic_max_f(float* a, float v) {
   else atomicMin(reinterpret_cast<unsigned int*>(a), __float_as_uint(v));
 }
 
+// blockIdx.y = channel c (at +c of every node), folded into minmax[2c], [2c+1]
 __global__ void range_kernel(const float* __restrict__ base, int dx, int dy, int dz, long long s0, long long s1,
                              long long s2, float* __restrict__ minmax) {
+  base += blockIdx.y;
+  minmax += 2 * blockIdx.y;
   float lo = __int_as_float(0x7f800000), hi = -lo;
   const long long total = (long long)dx * dy * dz;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < total;
@@ -428,8 +458,10 @@ __global__ void __launch_bounds__(kTile) debug_forward_simt_kernel(NetDesc net, 
   float x[3] = {0.f, 0.f, 0.f};
   if (j < q) { x[0] = __ldg(x01 + 3 * j); x[1] = __ldg(x01 + 3 * j + 1); x[2] = __ldg(x01 + 3 * j + 2); }
   encode_to_smem<F>(net, P, x, smem, t);
-  float v = mlp_forward_simt(net, P, smem, t);
-  if (j < q) y[j] = v;
+  float v[kMaxD];
+  mlp_forward_simt(net, P, smem, t, v);
+  if (j < q)
+    for (int c = 0; c < net.D; ++c) y[j * net.D + c] = v[c];
 }
 
 // ============================================================ host launchers
@@ -514,10 +546,11 @@ void launch_convert_f16_f32(const __half* src, float* dst, long long n, cudaStre
   count_launch();
 }
 
-void launch_range(const float* base, const int dims[3], const long long s[3], float* minmax, cudaStream_t st) {
+void launch_range(const float* base, const int dims[3], const long long s[3], int channels, float* minmax,
+                  cudaStream_t st) {
   long long total = (long long)dims[0] * dims[1] * dims[2];
   int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 8));
-  range_kernel<<<blocks, 256, 0, st>>>(base, dims[0], dims[1], dims[2], s[0], s[1], s[2], minmax);
+  range_kernel<<<dim3(blocks, channels), 256, 0, st>>>(base, dims[0], dims[1], dims[2], s[0], s[1], s[2], minmax);
   count_launch();
 }
 

@@ -33,46 +33,6 @@ namespace inr {
 
 using namespace tc;
 
-// Load this CTA's copy of the network (fp16 weight tiles, fp32 biases and output
-// layer), allocate TMEM and initialise the MMA-completion mbarrier.
-__device__ __forceinline__ uint32_t mlp_setup(const NetDesc& net, const float* __restrict__ P, uint8_t* smem,
-                                              const Layout& lay, bool ones_groups) {
-  const int t = threadIdx.x, warp = t >> 5;
-  const int H = net.H;
-  float* bias = reinterpret_cast<float*>(smem + lay.bias);
-  float* wout = reinterpret_cast<float*>(smem + lay.wout);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
-                 "r"(lay.ncols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  if (t == 0) {
-    mbar_init(smem_u32(smem + lay.mbar), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int k = 0; k < H; ++k) {
-    const int in = net.in_dim[k];
-    const float* W = P + net.w_off[k];
-    for (int e = t; e < 64 * in; e += blockDim.x) {
-      int n = e / in, i = e - n * in;
-      *reinterpret_cast<__half*>(smem + lay.w[k] + tile_off(lay.w_sbo[k], n, i)) = __float2half_rn(W[e]);
-    }
-    for (int n = t; n < 64; n += blockDim.x) bias[k * 64 + n] = net.bias ? P[net.b_off[k] + n] : 0.f;
-    if (ones_groups && lay.ones && t < kTileM) {  // constant ones group of h_k: column in_k = 1, in_k+1..+7 = 0
-      uint4 u = make_uint4(0x3C00u, 0u, 0u, 0u);   // half(1.0) in the low half of the first word
-      *reinterpret_cast<uint4*>(smem + lay.h[k] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[k] + (in >> 3) * 128) = u;
-    }
-  }
-  for (int i = t; i < 64; i += blockDim.x) wout[i] = P[net.w_off[H] + i];
-  if (t == 0) wout[64] = net.bias ? P[net.b_off[H]] : 0.f;
-  fence_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  return *tslot;
-}
-
 // Fit-kernel setup: TMEM allocation, barriers, the constant ones groups of
 // h_1..h_{H-1}, and one TMA bulk copy of the step's prepared weight image.
 __device__ __forceinline__ uint32_t mlp_setup_fit(const NetDesc& net, const uint8_t* wimg, uint8_t* smem,
@@ -131,8 +91,9 @@ __global__ void __launch_bounds__(256) prep_image_kernel(GroupArgs g, Layout lay
   float* bias = reinterpret_cast<float*>(dst + lay.bias);
   float* wout = reinterpret_cast<float*>(dst + lay.wout);
   for (int e = t; e < net.H * 64; e += 256) bias[e] = net.bias ? P[net.b_off[e / 64] + (e % 64)] : 0.f;
-  for (int i = t; i < 64; i += 256) wout[i] = P[net.w_off[net.H] + i];
-  if (t == 0) wout[64] = net.bias ? P[net.b_off[net.H]] : 0.f;
+  // output layer W_H [D][64] row-major, then b_H [D]
+  for (int i = t; i < net.D * 64; i += 256) wout[i] = P[net.w_off[net.H] + i];
+  if (t < net.D) wout[net.D * 64 + t] = net.bias ? P[net.b_off[net.H] + t] : 0.f;
 }
 
 __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
@@ -173,11 +134,12 @@ __device__ __forceinline__ void red_smem(float* red, unsigned long long* redx, b
   else atomicAdd(red + i, v);
 }
 
-template <int F>
+template <int F, int D>
 __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, FitScalars fs, Layout lay,
                                                                 float loss_scale, const uint8_t* __restrict__ featimg,
                                                                 const uint8_t* __restrict__ wimg,
                                                                 const float4* __restrict__ samples,
+                                                                const float4* __restrict__ targets,
                                                                 float* __restrict__ dfeat, int Bs) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
@@ -198,13 +160,13 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
 
   float* bias = reinterpret_cast<float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
-  // dW_H / db_H partial sums of this CTA: fp32, or exact int64 fixed point in the
-  // deterministic mode (the warps add in a run-dependent order)
+  // dW_H [D][64] / db_H [D] partial sums of this CTA: fp32, or exact int64 fixed
+  // point in the deterministic mode (the warps add in a run-dependent order)
   float* red = reinterpret_cast<float*>(smem + lay.red);
   unsigned long long* redx = reinterpret_cast<unsigned long long*>(smem + lay.red);
-  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [2][128] output-layer partial sums
+  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [D][2][128] output-layer partial sums
   const uint32_t mbar = smem_u32(smem + lay.mbar);
-  for (int i = t; i < 66; i += kFitThreads) redx[i] = 0ull;
+  for (int i = t; i < D * 65; i += kFitThreads) redx[i] = 0ull;
   const uint32_t tmem = mlp_setup_fit(net, wimg + (size_t)m * lay.img_bytes, smem, lay);
   const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   uint32_t phase = 0;
@@ -222,7 +184,13 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
     const int i = tile * kTileM + r;
     const bool valid = i < total;
     const bool is_b = i >= fs.B_u;
-    const float target = valid ? samples[(size_t)m * Bs + i].w : 0.f;
+    float target[D];
+    if constexpr (D == 1) {
+      target[0] = valid ? samples[(size_t)m * Bs + i].w : 0.f;
+    } else {
+      const float4 tg = valid ? targets[(size_t)m * Bs + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      target[0] = tg.x; target[1] = tg.y; target[2] = tg.z;
+    }
     const int b = it & 1;
     const uint32_t h0 = hbuf[b];
     if (t == 0 && tile + (int)gridDim.x < ntiles) {   // prefetch the next tile into the other buffer
@@ -266,26 +234,36 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
 #pragma unroll
         for (int j = 0; j < 4; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], r, hf * 4 + j, z + 8 * j);
       } else {
-        float yp = 0.f;
+        float yp[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) yp[c] = 0.f;
 #pragma unroll
         for (int n = 0; n < 32; ++n) {
           hH[n] = z[n];
-          yp = fmaf(wout[cb + n], z[n], yp);
+#pragma unroll
+          for (int c = 0; c < D; ++c) yp[c] = fmaf(wout[c * 64 + cb + n], z[n], yp[c]);
         }
-        ypart[hf * kTileM + r] = yp;
+#pragma unroll
+        for (int c = 0; c < D; ++c) ypart[(2 * c + hf) * kTileM + r] = yp[c];
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
-    // ---- output layer (fp32, CUDA cores) and Eq. 2
-    const float y = wout[64] + ypart[r] + ypart[kTileM + r];
-    const float d = y - target;
-    const float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
-    const float dy = is_b ? lam * sg / (float)max(B_b, 1) : (1.f - lam) * sg / (float)fs.B_u;
+    // ---- output layer (fp32, CUDA cores) and Eq. 2, L1 pooled over the D channels [R28]
+    float dy[D];
+    double ad = 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      const float y = wout[D * 64 + c] + ypart[(2 * c) * kTileM + r] + ypart[(2 * c + 1) * kTileM + r];
+      const float d = y - target[c];
+      const float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
+      dy[c] = is_b ? lam * sg / (float)(max(B_b, 1) * D) : (1.f - lam) * sg / (float)(fs.B_u * D);
+      ad += fabs((double)d);
+    }
     if (hf == 0) {
-      double au = (valid && !is_b) ? fabs((double)d) : 0.0;
-      double ab = (valid && is_b) ? fabs((double)d) : 0.0;
+      double au = (valid && !is_b) ? ad : 0.0;
+      double ab = (valid && is_b) ? ad : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         au += __shfl_xor_sync(0xffffffffu, au, o);
@@ -295,22 +273,30 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
         if (au != 0.0) atomicAdd(md.acc + 0, au);
         if (ab != 0.0) atomicAdd(md.acc + 1, ab);
       }
-      float s = dy;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) red_smem(red, redx, det, 64, s);               // db_H
+      for (int c = 0; c < D; ++c) {
+        float s = dy[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red_smem(red, redx, det, D * 64 + c, s);   // db_H[c]
+      }
     }
-    {   // dW_H[n] = sum_s dy_s h_H[s][n] for this thread's 32 columns
+#pragma unroll
+    for (int c = 0; c < D; ++c) {   // dW_H[c][n] = sum_s dy_c,s h_H[s][n] for this thread's 32 columns
       float v[32];
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[n] = dy * hH[n];
-      red_smem(red, redx, det, cb + lane, warp_transpose_reduce32(v, lane));
+      for (int n = 0; n < 32; ++n) v[n] = dy[c] * hH[n];
+      red_smem(red, redx, det, c * 64 + cb + lane, warp_transpose_reduce32(v, lane));
     }
-    {   // dz_{H-1} = dy W_H * 1[z_{H-1} > 0], scaled by 2^s
+    {   // dz_{H-1} = (sum_c dy_c W_H[c]) * 1[z_{H-1} > 0], scaled by 2^s
       float dz[32];
-      const float sdy = dy * loss_scale;
 #pragma unroll
-      for (int n = 0; n < 32; ++n) dz[n] = ((mask[H - 1] >> n) & 1u) ? sdy * wout[cb + n] : 0.f;
+      for (int n = 0; n < 32; ++n) {
+        float a = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) a = fmaf(dy[c] * loss_scale, wout[c * 64 + cb + n], a);
+        dz[n] = ((mask[H - 1] >> n) & 1u) ? a : 0.f;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dz + 8 * j);
     }
@@ -397,11 +383,11 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
   __syncthreads();
   if (!first) {
     if (det) {
-      for (int n = t; n < 64; n += kFitThreads) atomicAdd(GX + net.w_off[H] + n, redx[n]);
-      if (t == 0 && net.bias) atomicAdd(GX + net.b_off[H], redx[64]);
+      for (int n = t; n < D * 64; n += kFitThreads) atomicAdd(GX + net.w_off[H] + n, redx[n]);
+      if (t < D && net.bias) atomicAdd(GX + net.b_off[H] + t, redx[D * 64 + t]);
     } else {
-      for (int n = t; n < 64; n += kFitThreads) atomicAdd(G + net.w_off[H] + n, red[n]);
-      if (t == 0 && net.bias) atomicAdd(G + net.b_off[H], red[64]);
+      for (int n = t; n < D * 64; n += kFitThreads) atomicAdd(G + net.w_off[H] + n, red[n]);
+      if (t < D && net.bias) atomicAdd(G + net.b_off[H] + t, red[D * 64 + t]);
     }
   }
   mlp_teardown(tmem, lay);
@@ -412,7 +398,8 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
 // otherwise the forward-only layout (64 TMEM columns).
 static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   memset(&L, 0, sizeof L);
-  if (net.LF % 16 != 0 || net.LF > 64 || net.H < 1 || net.H > kMaxLayers - 1 || net.D != 1) return false;
+  if (net.LF % 16 != 0 || net.LF > 64 || net.H < 1 || net.H > kMaxLayers - 1 || (net.D != 1 && net.D != 3))
+    return false;
   L.ones = (net.bias && train) ? 8 : 0;
   uint32_t off = 0;
   auto take = [&](uint32_t bytes, uint32_t align) {
@@ -427,7 +414,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
     L.w[k] = take(64 * net.in_dim[k] * 2, 1024);
   }
   L.bias = take(net.H * 64 * 4, 16);
-  L.wout = take(68 * 4, 16);
+  L.wout = take((net.D * 64 + 4) * 4, 16);
   L.img_bytes = (off + 15) / 16 * 16;
   off = L.img_bytes;
   if (train) {   // every activation tile is kept for the backward pass
@@ -447,8 +434,8 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   if (train) L.h0b = take(L.feat_tile_bytes, 1024);
   L.dz_sbo = 8 * 128;
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
-  L.red = take(66 * 8, 16);
-  L.ypart = take(2 * kTileM * 4, 16);
+  L.red = take((net.D * 65 + 1) * 8, 16);
+  L.ypart = take(net.D * 2 * kTileM * 4, 16);
   L.mbar = take(8, 8);
   L.mbar_img = take(8, 8);
   L.mbar_feat[0] = take(8, 8);
@@ -505,7 +492,7 @@ void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStrea
 }
 
 void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
-                   const float4* samples, float* dfeat, int Bs, cudaStream_t st) {
+                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L)) return;
   const int total = fs.B_u + fs.B_b;
@@ -514,14 +501,15 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
   int per_model = std::max(1, std::min(ntiles, (slots + nmodels - 1) / nmodels));
   dim3 grid(per_model, nmodels);
   float ls = loss_scale_for(fs.B_u);
-  switch (g.net.F) {
-#define CASE_F(FF)                                                                                   \
-  case FF:                                                                                           \
-    cudaFuncSetAttribute(mlp_fit_kernel<FF>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);  \
-    mlp_fit_kernel<FF><<<grid, kFitThreads, L.bytes, st>>>(g, fs, L, ls, featimg, wimg, samples, dfeat, Bs); \
+  switch (g.net.F * 10 + g.net.D) {
+#define CASE_FD(FF, DD)                                                                                   \
+  case FF * 10 + DD:                                                                                      \
+    cudaFuncSetAttribute(mlp_fit_kernel<FF, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
+    mlp_fit_kernel<FF, DD><<<grid, kFitThreads, L.bytes, st>>>(g, fs, L, ls, featimg, wimg, samples, targets, \
+                                                                dfeat, Bs);                                \
     break;
-    CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
-#undef CASE_F
+    CASE_FD(1, 1) CASE_FD(2, 1) CASE_FD(4, 1) CASE_FD(8, 1) CASE_FD(1, 3) CASE_FD(2, 3) CASE_FD(4, 3) CASE_FD(8, 3)
+#undef CASE_FD
     default: break;
   }
   count_launch();
@@ -550,7 +538,7 @@ struct FwdArgs {
   const uint8_t* wimg;   // prepared weight images, one per model slot (prep_image_kernel)
 };
 
-template <int F, int MODE>
+template <int F, int MODE, int D>
 __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
@@ -650,7 +638,9 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
     fence_async_smem();
     fence_before();
     __syncthreads();
-    float y = wout[64];
+    float y[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) y[c] = wout[D * 64 + c];
     for (int k = 0; k < H; ++k) {
       if (t == 0) {
         fence_after();
@@ -676,24 +666,36 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
       if (k + 1 < H) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, jj, z + 8 * jj);
-      } else {   // the 64 -> 1 output layer, fp32 on CUDA cores
+      } else {   // the 64 -> D output layer, fp32 on CUDA cores
 #pragma unroll
-        for (int n = 0; n < 64; ++n) y = fmaf(wout[n], z[n], y);
+        for (int n = 0; n < 64; ++n) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) y[c] = fmaf(wout[c * 64 + n], z[n], y[c]);
+        }
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
     if constexpr (MODE == 0) {
-      if (valid) a.y[j] = y;
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) a.y[j * D + c] = y[c];
+      }
     } else {
       double e = 0.0;
       if (valid) {
-        const float v = fmaf(y, md.vrange, md.vmin);
-        a.out[dst] = v;
-        if (MODE == 1 && a.ref) {
-          const double dd = ((double)v - (double)__ldg(a.ref + dst)) / (double)md.vrange;
-          e = dd * dd;
+        if constexpr (MODE == 2) dst *= D;   // query outputs: q x D, channels interleaved
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const float v = fmaf(y[c], md.vrange[c], md.vmin[c]);
+          a.out[dst + c] = v;
+          if (MODE == 1 && a.ref) {
+            // a constant channel (vrange 0) is 0 in normalized units on both sides
+            const double dd =
+                md.vrange[c] > 0.f ? ((double)v - (double)__ldg(a.ref + dst + c)) / (double)md.vrange[c] : 0.0;
+            e += dd * dd;
+          }
         }
       }
       if (MODE == 1 && a.sse) {
@@ -717,14 +719,14 @@ static void launch_forward(const GroupArgs& g, const FwdArgs& a0, long long ntil
   prep_image_kernel<<<dim3(g.nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg);
   count_launch();
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles_hint, 148ll * L.ctas_per_sm));
-  switch (g.net.F) {
-#define CASE_F(FF)                                                                                              \
-  case FF:                                                                                                      \
-    cudaFuncSetAttribute(forward_tc_kernel<FF, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
-    forward_tc_kernel<FF, MODE><<<grid, kThreads, L.bytes, st>>>(g, a, L);                                     \
+  switch (g.net.F * 10 + g.net.D) {
+#define CASE_FD(FF, DD)                                                                                             \
+  case FF * 10 + DD:                                                                                                \
+    cudaFuncSetAttribute(forward_tc_kernel<FF, MODE, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
+    forward_tc_kernel<FF, MODE, DD><<<grid, kThreads, L.bytes, st>>>(g, a, L);                                     \
     break;
-    CASE_F(1) CASE_F(2) CASE_F(4) CASE_F(8)
-#undef CASE_F
+    CASE_FD(1, 1) CASE_FD(2, 1) CASE_FD(4, 1) CASE_FD(8, 1) CASE_FD(1, 3) CASE_FD(2, 3) CASE_FD(4, 3) CASE_FD(8, 3)
+#undef CASE_FD
     default: break;
   }
   count_launch();

@@ -52,7 +52,8 @@ void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q
                               cudaStream_t st);
 void launch_convert_f32_f16(const float* src, __half* dst, long long n, cudaStream_t st);
 void launch_convert_f16_f32(const __half* src, float* dst, long long n, cudaStream_t st);
-void launch_range(const float* base, const int dims[3], const long long s[3], float* minmax, cudaStream_t st);
+void launch_range(const float* base, const int dims[3], const long long s[3], int channels, float* minmax,
+                  cudaStream_t st);
 void launch_debug_encode(const NetDesc& net, const float* P, const float* x01, long long q, uint32_t* idx,
                          float* feat, cudaStream_t st);
 void launch_debug_forward_simt(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
@@ -73,6 +74,7 @@ struct LmWorkspace {
   uint8_t* featimg;  // [model][Bs/128] fp16 h_0 tile images
   float* dfeat;      // [model][level][Bs][F] fp32
   uint8_t* wimg;     // [model] fp16 weight images (tiles, biases, output layer)
+  float4* targets;   // [model][Bs] (t_0, t_1, t_2, 0) for vector fields, else null
   FeatGeom geom;
   uint32_t img_bytes;
   int Bs;            // per-model sample stride (multiple of 128)
@@ -86,7 +88,7 @@ void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, co
 void launch_encode_bwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 bool tc_supported(const NetDesc& net);
 void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
-                   const float4* samples, float* dfeat, int Bs, cudaStream_t st);
+                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st);
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
 void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,

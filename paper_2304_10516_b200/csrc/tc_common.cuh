@@ -23,9 +23,9 @@ struct Layout {
   uint32_t h_sbo[kMaxLayers];
   uint32_t dz, dz_sbo;           // fp16 dz tile [128 x 64]
   uint32_t bias;                 // fp32 [H][64]
-  uint32_t wout;                 // fp32 W_H[64], then b_H
-  uint32_t red;                  // dW_H[64], db_H partials (fp32 or int64 fixed point)
-  uint32_t ypart;                // fp32 [2][128] output-layer partial sums (fit)
+  uint32_t wout;                 // fp32 W_H[D][64], then b_H[D]
+  uint32_t red;                  // dW_H[D][64], db_H[D] partials (fp32 or int64 fixed point)
+  uint32_t ypart;                // fp32 [D][2][128] output-layer partial sums (fit)
   uint32_t mbar;                 // 8 B: MMA completion
   uint32_t mbar_img;             // 8 B: weight-image bulk copy (fit)
   uint32_t mbar_feat[2];         // 8 B each: feature-tile bulk copies (fit, double buffered)

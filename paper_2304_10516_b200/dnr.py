@@ -64,12 +64,16 @@ def _dev():
 
 
 def allreduce_range(vmin, vmax):
-    """Global (vmin, vmax) over ranks: all-reduce MIN and MAX."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
-        return float(vmin), float(vmax)
-    t = torch.tensor([float(vmin), -float(vmax)], dtype=torch.float64, device=_dev())
-    dist.all_reduce(t, op=dist.ReduceOp.MIN)
-    return float(t[0]), float(-t[1])
+    """Global (vmin, vmax) over ranks: all-reduce MIN and MAX; scalars,
+    or per-channel lists for vector fields."""
+    vec = hasattr(vmin, "__len__")
+    lo = [float(v) for v in (vmin if vec else [vmin])]
+    hi = [float(v) for v in (vmax if vec else [vmax])]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        t = torch.tensor(lo + [-v for v in hi], dtype=torch.float64, device=_dev())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        lo, hi = t[:len(lo)].tolist(), [-v for v in t[len(lo):].tolist()]
+    return (lo, hi) if vec else (lo[0], hi[0])
 
 
 def allreduce_sum(values):
@@ -159,39 +163,48 @@ class DNR:
         for b in self.block_ids:
             o = block_origin(b, self.global_dims, self.n)
             self.models.append(inr.inr_create(cfg, inr.make_block(o, self.n, self.global_dims), self.device))
+        self.D = int(cfg.out_dim)
         self.vmin, self.vmax = 0.0, 1.0
 
     def local_dims(self):
         """(nx, ny, nz) of the local sub-volume."""
         return tuple(h - l + 1 for l, h in zip(self.lo, self.hi))
 
+    def _strides(self, nx, ny):
+        D = self.D
+        return (D, D * nx, D * nx * ny)
+
     def views(self, local_volume):
-        """One view per local block into the local sub-volume (zero-copy)."""
-        nz, ny, nx = local_volume.shape
+        """One view per local block into the local sub-volume [z, y, x] or, for
+        vector fields, [z, y, x, c] (zero-copy)."""
+        nz, ny, nx = local_volume.shape[:3]
         assert (nx, ny, nz) == self.local_dims(), (local_volume.shape, self.local_dims())
-        v = self.inr.make_view(local_volume.data_ptr(), self.lo, (nx, ny, nz), (1, nx, nx * ny))
+        v = self.inr.make_view(local_volume.data_ptr(), self.lo, (nx, ny, nz), self._strides(nx, ny), self.D)
         return [v] * len(self.models)
 
     def value_range(self, local_volume, stream=0):
         """Min/max over this rank's core nodes (libinr range kernel), then the
         all-reduce (a1)."""
-        nz, ny, nx = local_volume.shape
-        mm = torch.tensor([float("inf"), float("-inf")], device=local_volume.device)
+        nz, ny, nx = local_volume.shape[:3]
+        mm = torch.tensor([float("inf"), float("-inf")] * self.D, device=local_volume.device)
         # core nodes only: the high ghost layer belongs to the next rank's blocks
         core_hi = [min(h, self.hi[d] if self.hi[d] == self.global_dims[d] - 1 else self.hi[d] - 1)
                    for d, h in enumerate(self.hi)]
         dims = tuple(core_hi[d] - self.lo[d] + 1 for d in range(3))
-        v = self.inr.make_view(local_volume.data_ptr(), self.lo, dims, (1, nx, nx * ny))
+        v = self.inr.make_view(local_volume.data_ptr(), self.lo, dims, self._strides(nx, ny), self.D)
         self.inr.inr_value_range(v, mm.data_ptr(), stream)
         torch.cuda.current_stream().synchronize()
-        lo, hi = mm.tolist()
-        self.vmin, self.vmax = allreduce_range(lo, hi)
+        r = mm.tolist()
+        if self.D == 1:
+            self.vmin, self.vmax = allreduce_range(r[0], r[1])
+        else:
+            self.vmin, self.vmax = allreduce_range(r[0::2], r[1::2])
         return self.vmin, self.vmax
 
     def fit(self, local_volume, steps, batch, opts, stream=0, report=True):
         """inr_fit_group over the local blocks (no communication), then the
         metadata all-gather when a report is requested."""
-        opts.vmin, opts.vmax = self.vmin, self.vmax
+        opts.set_range(self.vmin, self.vmax)
         reps = self.inr.inr_fit_group(self.models, self.views(local_volume), steps, batch, opts, stream, report)
         if not report:
             return None
@@ -202,8 +215,9 @@ class DNR:
     def decode_grid_local(self, out, scale=1, ref=None, sse=None, stream=0):
         """Decode every local block at `scale` x resolution into `out`, a tensor
         [z, y, x] covering the local cores at that resolution (strided writes,
-        no copies); optional fused SSE against `ref` (same layout)."""
-        nz, ny, nx = out.shape
+        no copies); optional fused SSE against `ref` (same layout).  Vector
+        fields: out is [z, y, x, c]."""
+        nz, ny, nx = out.shape[:3]
         res = tuple(int(b * scale) for b in self.n)
         for b, m in zip(self.block_ids, self.models):
             o = block_origin(b, self.global_dims, self.n)
@@ -212,7 +226,7 @@ class DNR:
             r = tuple(min(res[d], (self.global_dims[d] - o[d]) * scale) for d in range(3))
             base = out[off[2]:, off[1]:, off[0]:]
             refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
-            self.inr.inr_decode_grid(m, r, base.data_ptr(), (1, nx, nx * ny), refp,
+            self.inr.inr_decode_grid(m, r, base.data_ptr(), self._strides(nx, ny), refp,
                                      sse.data_ptr() if sse is not None else None, stream)
 
     def core_box(self):

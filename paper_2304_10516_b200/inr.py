@@ -51,7 +51,17 @@ class inr_fit_opts(ctypes.Structure):
     _fields_ = [("lambda_", ctypes.c_double), ("boundary_batch", ctypes.c_int32), ("lr0", ctypes.c_double),
                 ("lr_decay", ctypes.c_double), ("lr_step", ctypes.c_int32), ("beta1", ctypes.c_double),
                 ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("vmin", ctypes.c_double),
-                ("vmax", ctypes.c_double), ("target_psnr", ctypes.c_double), ("check_interval", ctypes.c_int32)]
+                ("vmax", ctypes.c_double), ("target_psnr", ctypes.c_double), ("check_interval", ctypes.c_int32),
+                ("vmin_c", ctypes.c_double * 3), ("vmax_c", ctypes.c_double * 3)]
+
+    def set_range(self, lo, hi):
+        """Scalar range (scalar fields) or per-channel sequences (vector fields)."""
+        if hasattr(lo, "__len__"):
+            for c in range(len(lo)):
+                self.vmin_c[c], self.vmax_c[c] = float(lo[c]), float(hi[c])
+            self.vmin, self.vmax = float(lo[0]), float(hi[0])
+        else:
+            self.vmin, self.vmax = float(lo), float(hi)
 
 
 class inr_fit_report(ctypes.Structure):
@@ -62,7 +72,7 @@ class inr_fit_report(ctypes.Structure):
 
 class inr_view(ctypes.Structure):
     _fields_ = [("base", ctypes.c_void_p), ("lo", ctypes.c_int64 * 3), ("dims", ctypes.c_int32 * 3),
-                ("stride", ctypes.c_int64 * 3)]
+                ("stride", ctypes.c_int64 * 3), ("channels", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -138,8 +148,10 @@ def make_block(origin, n, global_dims):
     return inr_block((ctypes.c_int64 * 3)(*origin), (ctypes.c_int32 * 3)(*n), (ctypes.c_int64 * 3)(*global_dims))
 
 
-def make_view(base_ptr, lo, dims, stride):
-    return inr_view(base_ptr, (ctypes.c_int64 * 3)(*lo), (ctypes.c_int32 * 3)(*dims), (ctypes.c_int64 * 3)(*stride))
+def make_view(base_ptr, lo, dims, stride, channels=1):
+    """Strides in elements per node; a vector field (channels = 3) stores channel c at +c."""
+    return inr_view(base_ptr, (ctypes.c_int64 * 3)(*lo), (ctypes.c_int32 * 3)(*dims), (ctypes.c_int64 * 3)(*stride),
+                    channels)
 
 
 def inr_fit_opts_default():

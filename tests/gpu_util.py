@@ -23,8 +23,10 @@ def gpu_volume(vol_np):
 
 
 def whole_view(vol_t):
-    nz, ny, nx = vol_t.shape
-    return inr.make_view(vol_t.data_ptr(), (0, 0, 0), (nx, ny, nz), (1, nx, nx * ny))
+    """View of a whole [z, y, x] scalar or [z, y, x, c] vector volume."""
+    nz, ny, nx = vol_t.shape[:3]
+    D = vol_t.shape[3] if vol_t.dim() == 4 else 1
+    return inr.make_view(vol_t.data_ptr(), (0, 0, 0), (nx, ny, nz), (D, D * nx, D * nx * ny), D)
 
 
 def make_gpu_model(blk, seed, **kw):

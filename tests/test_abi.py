@@ -72,7 +72,7 @@ def test_argument_validation_without_device():
     for kw in bad:
         cfg = inr.make_config(**{**dict(levels=4, log2_table_size=10), **kw})
         assert L.inr_create(ctypes.byref(cfg), ctypes.byref(blk), 0, ctypes.byref(h)) == inr.INR_ERR_INVALID_ARG
-    for kw in (dict(features=3), dict(mlp_width=32), dict(out_dim=3), dict(levels=16, features=8)):
+    for kw in (dict(features=3), dict(mlp_width=32), dict(out_dim=2), dict(levels=16, features=8)):
         cfg = inr.make_config(**{**dict(levels=4, log2_table_size=10), **kw})
         assert L.inr_create(ctypes.byref(cfg), ctypes.byref(blk), 0, ctypes.byref(h)) == inr.INR_ERR_UNSUPPORTED
     cfg = inr.make_config(levels=4, log2_table_size=10)

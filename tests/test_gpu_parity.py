@@ -169,6 +169,9 @@ def linear_regime(cfg, blk, vol, seed, batch, boundary_batch, rng):
     y, cache = o_fit.forward(om, x)
     assert all(float(z.min()) >= 0.5 for z in cache[3][:-1]) or not cfg.mlp_bias
     assert all(float(z.min()) > 0 for z in cache[3][:-1])
+    if vol.ndim == 4:    # vector field: per-channel ranges
+        lo = vol.max(axis=(0, 1, 2)).astype(np.float64) - y.min(axis=0) + 1.0 + 0.01 * np.abs(y).max(axis=0)
+        return p, lo, lo + 1.0, om
     lo = float(vol.max()) - float(y.min()) + 1.0 + 0.01 * float(np.abs(y).max())
     return p, lo, lo + 1.0, om
 

@@ -118,3 +118,12 @@ def test_vector_gradients_match_central_differences():
             fd[j] = (fp - fm) / (2 * h)
         assert np.max(np.abs(g - fd) / np.maximum(np.abs(fd), 1e-3)) < 1e-4
         checked += 1
+
+
+def test_sse_constant_channel_contributes_zero():
+    """a constant channel normalizes to 0 on both sides, so it adds
+    nothing to the pooled SSE; the other channels add ((p - r) / range)^2."""
+    pred = np.array([[1.0, 5.0, 2.0], [3.0, 5.0, 0.0]])
+    ref = np.array([[0.0, 5.0, 1.0], [3.0, 5.0, 2.0]])
+    s = decode.sse_normalized(pred, ref, np.array([0.0, 5.0, 0.0]), np.array([2.0, 5.0, 4.0]))
+    assert s == (1 / 2) ** 2 + (1 / 4) ** 2 + (2 / 4) ** 2
