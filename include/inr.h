@@ -209,6 +209,13 @@ INR_API inr_status inr_decode_group(const inr_model* const* models, int32_t nmod
 INR_API inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
                            const int64_t* out_stride, const float* ref, double* sse_dev,
                            cudaStream_t stream);
+/* The same for only the first count[d] <= res[d] lattice points per axis
+ * (j_d < count_d, still at x_j = fl32(j / res_d)): a block at the upper domain
+ * face whose remaining nodes N - o are fewer than n decodes res = n,
+ * count = N - o, i.e. exactly its nodes (count NULL = res). */
+INR_API inr_status inr_decode_grid_part(const inr_model* m, const int32_t res[3], const int32_t count[3],
+                                float* out, const int64_t* out_stride, const float* ref, double* sse_dev,
+                                cudaStream_t stream);
 
 /* Min/max over the nodes of a view: atomically
  * folds into minmax_dev[2c] (min) and minmax_dev[2c+1] (max) of every channel c
@@ -242,6 +249,39 @@ INR_API inr_status cache_bytes(const inr_cache* c, int64_t* bytes);
  * valid until that slot is evicted; inr_fit/inr_reset on them -> INR_ERR_STATE). */
 INR_API inr_status cache_get(const inr_cache* c, int32_t i, int64_t* timestep, const inr_model* const** blocks,
                      int32_t* nblocks);
+
+/* ---- pathlines over the window (NEXT-2) ----
+ * Positions are global node coordinates (float64), velocities node units per
+ * unit time.  Classical RK4 with a fixed step: each window interval
+ * [t_i, t_{i+1}] is split into k_i = max(1, ceil((t_{i+1} - t_i)/dt - 1e-12))
+ * equal substeps; the velocity is trilinear in space (clamped indices, per
+ * channel) and linear in time between the two bounding elements [R29-R31].
+ * A seed ends when a substep would put its result or any RK stage position
+ * outside [0, N-1]^3 (OUT_OF_DOMAIN; a seed outside at t_0 gets no vertex),
+ * after max_steps substeps (MAX_STEPS), or at the window's end.
+ * Outputs (device): vertices[M][max_steps + 1][5] rows (x, y, z, t, |V|) —
+ * only the first counts[s] rows of seed s are written — counts[M], reasons[M].
+ * Stream-ordered and asynchronous. */
+enum { INR_PATH_WINDOW_EXHAUSTED = 0, INR_PATH_OUT_OF_DOMAIN = 1, INR_PATH_MAX_STEPS = 2 };
+/* Trace on explicit velocity grids: grids (host array of ngrids >= 2 device
+ * pointers) each [dims2][dims1][dims0][3] fp32, channels interleaved, at
+ * strictly increasing times (host); every value is multiplied by sign. */
+INR_API inr_status inr_trace_grids(const float* const* grids, const double* times, int32_t ngrids,
+                           const int64_t dims[3], double sign, const double* seeds, int32_t nseeds, double dt,
+                           int32_t max_steps, double* vertices, int32_t* counts, int32_t* reasons,
+                           cudaStream_t stream);
+/* Trace over a cached window of vector-field (out_dim 3) models, each element
+ * holding every block of the volume, at times = the cached timesteps.
+ * window_ops: INR_WINDOW_REVERSE (element i -> W-1-i, time tau_i = t_{W-1} -
+ * t_{W-1-i}) and/or INR_WINDOW_NEGATE (every value times -1) — so
+ * INR_WINDOW_REVERSE | INR_WINDOW_NEGATE is the paper's backward tracing
+ * pathline(negate(reverse(W))).  Elements are decoded to the
+ * global grid on demand, at most two resident (2 x 12 N^3 bytes of
+ * stream-ordered scratch). */
+enum { INR_WINDOW_REVERSE = 1, INR_WINDOW_NEGATE = 2 };
+INR_API inr_status inr_pathlines(const inr_cache* c, int32_t window_ops, const double* seeds, int32_t nseeds,
+                         double dt, int32_t max_steps, double* vertices, int32_t* counts, int32_t* reasons,
+                         cudaStream_t stream);
 
 /* ---- parity / test surface ---- */
 /* Copy n = inr_param_count floats of parameters / last-step gradients / Adam m /

@@ -61,9 +61,10 @@ extern "C" const char* inr_last_error(void) { return g_err.c_str(); }
 
 // ------------------------------------------------------------------ profiling
 enum ProfKind { PK_STEP_BEGIN, PK_FIT_FP32, PK_SAMPLE, PK_ENCODE_FWD, PK_PREP, PK_MLP_TC, PK_ENCODE_BWD, PK_ADAM,
-                PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE, PK_COUNT };
+                PK_DECODE_GRID, PK_DECODE_QUERY, PK_PROBE, PK_RANGE, PK_PATHLINE, PK_COUNT };
 static const char* kProfNames[PK_COUNT] = {"step_begin", "fit_fp32", "sample", "encode_fwd", "prep_image", "mlp_tc",
-                                           "encode_bwd", "adam", "decode_grid", "decode_query", "probe", "range"};
+                                           "encode_bwd", "adam", "decode_grid", "decode_query", "probe", "range",
+                                           "pathline"};
 struct ProfRec { int kind; cudaEvent_t a, b; };
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_event_pool;
@@ -697,12 +698,14 @@ extern "C" inr_status inr_fit_group(inr_model* const* models, const inr_view* vi
 }
 
 // ------------------------------------------------------------------ decode
-extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
-                                      const int64_t* out_stride, const float* ref, double* sse_dev,
-                                      cudaStream_t st) {
+extern "C" inr_status inr_decode_grid_part(const inr_model* m, const int32_t res[3], const int32_t count[3],
+                                           float* out, const int64_t* out_stride, const float* ref, double* sse_dev,
+                                           cudaStream_t st) {
   if (!m || !res || !out) return fail(INR_ERR_INVALID_ARG, "NULL argument");
-  for (int d = 0; d < 3; ++d)
+  for (int d = 0; d < 3; ++d) {
     if (res[d] < 1 || res[d] > (1 << 20)) return fail(INR_ERR_INVALID_ARG, "res must be in 1..2^20");
+    if (count && (count[d] < 1 || count[d] > res[d])) return fail(INR_ERR_INVALID_ARG, "count must be in 1..res");
+  }
   if (ref && !sse_dev) return fail(INR_ERR_INVALID_ARG, "ref given without sse_dev");
   CK(cudaSetDevice(m->device));
   inr_status s = ensure_device_params(m, st);
@@ -714,14 +717,23 @@ extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], 
     os[0] = D; os[1] = D * res[0]; os[2] = D * res[0] * res[1];
   }
   int r[3] = {res[0], res[1], res[2]};
+  int c[3] = {count ? count[0] : res[0], count ? count[1] : res[1], count ? count[2] : res[2]};
   ModelDev md = model_dev(m);
   {
     ProfScope p(PK_DECODE_GRID, st);
-    if (m->cfg.precision == INR_PREC_FP16_MLP) launch_decode_grid_tc(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
-    else launch_decode_grid_simt(m->net, md, r, out, os, ref, ref ? sse_dev : nullptr, st);
+    if (m->cfg.precision == INR_PREC_FP16_MLP)
+      launch_decode_grid_tc(m->net, md, r, c, out, os, ref, ref ? sse_dev : nullptr, st);
+    else
+      launch_decode_grid_simt(m->net, md, r, c, out, os, ref, ref ? sse_dev : nullptr, st);
   }
   CK_LAUNCH("decode_grid");
   return INR_OK;
+}
+
+extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], float* out,
+                                      const int64_t* out_stride, const float* ref, double* sse_dev,
+                                      cudaStream_t st) {
+  return inr_decode_grid_part(m, res, nullptr, out, out_stride, ref, sse_dev, st);
 }
 
 static inr_status decode_group_impl(const inr_model* const* models, int32_t nmodels, const float* xyz, int64_t q,
@@ -1056,3 +1068,121 @@ extern "C" inr_status cache_get(const inr_cache* c, int32_t i, int64_t* timestep
   if (nblocks) *nblocks = (int32_t)s.cmodels.size();
   return INR_OK;
 }
+
+// ------------------------------------------------------------------ pathlines
+// NEXT-2: RK4 over a window of decoded
+// velocity grids, at most two resident, one launch per interval.
+static inr_status check_path_args(const void* seeds, int32_t nseeds, double dt, int32_t max_steps, const void* vert,
+                                  const void* counts, const void* reasons) {
+  if (nseeds < 0) return fail(INR_ERR_INVALID_ARG, "nseeds must be >= 0");
+  if (nseeds > 0 && (!seeds || !vert || !counts || !reasons)) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (!(dt > 0.0)) return fail(INR_ERR_INVALID_ARG, "dt must be > 0");
+  if (max_steps < 0) return fail(INR_ERR_INVALID_ARG, "max_steps must be >= 0");
+  return INR_OK;
+}
+
+extern "C" inr_status inr_trace_grids(const float* const* grids, const double* times, int32_t ngrids,
+                                      const int64_t dims[3], double sign, const double* seeds, int32_t nseeds,
+                                      double dt, int32_t max_steps, double* vertices, int32_t* counts,
+                                      int32_t* reasons, cudaStream_t st) {
+  if (!grids || !times || !dims) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (ngrids < 2) return fail(INR_ERR_INVALID_ARG, "a pathline window needs at least two grids");
+  inr_status s = check_path_args(seeds, nseeds, dt, max_steps, vertices, counts, reasons);
+  if (s) return s;
+  for (int i = 0; i + 1 < ngrids; ++i)
+    if (!(times[i + 1] > times[i])) return fail(INR_ERR_INVALID_ARG, "times must be strictly increasing");
+  long long n[3] = {dims[0], dims[1], dims[2]};
+  for (int d = 0; d < 3; ++d)
+    if (n[d] < 1) return fail(INR_ERR_INVALID_ARG, "dims must be >= 1");
+  if (nseeds == 0) return INR_OK;
+  ProfScope p(PK_PATHLINE, st);
+  launch_path_init(grids[0], grids[1], n, times[0], sign, seeds, nseeds, max_steps, vertices, counts, reasons, st);
+  for (int i = 0; i + 1 < ngrids; ++i)
+    launch_path_interval(grids[i], grids[i + 1], n, times[i], times[i + 1], dt, sign, max_steps, nseeds, vertices,
+                         counts, reasons, st);
+  launch_path_finish(nseeds, reasons, st);
+  CK_LAUNCH("pathlines");
+  return INR_OK;
+}
+
+// Decode every block of one window element into the global velocity grid.
+static inr_status decode_element(const CacheSlot& slot, float* grid, const int64_t N[3], cudaStream_t st) {
+  const inr_model* m0 = slot.cmodels[0];
+  const int64_t B[3] = {(N[0] + m0->blk.n[0] - 1) / m0->blk.n[0], (N[1] + m0->blk.n[1] - 1) / m0->blk.n[1],
+                        (N[2] + m0->blk.n[2] - 1) / m0->blk.n[2]};
+  if ((int64_t)slot.cmodels.size() != B[0] * B[1] * B[2])
+    return fail(INR_ERR_INVALID_ARG, "a window element must hold every block of the volume");
+  const int64_t os[3] = {3, 3 * N[0], 3 * N[0] * N[1]};
+  for (const inr_model* m : slot.cmodels) {
+    if (m->net.D != 3) return fail(INR_ERR_INVALID_ARG, "pathlines need vector-field (out_dim 3) models");
+    int32_t res[3], cnt[3];
+    int64_t off = 0;
+    for (int d = 0; d < 3; ++d) {
+      if (m->blk.global_dims[d] != N[d] || m->blk.n[d] != m0->blk.n[d])
+        return fail(INR_ERR_INVALID_ARG, "window element models must tile one volume");
+      res[d] = m->blk.n[d];
+      cnt[d] = (int32_t)std::min<int64_t>(m->blk.n[d], N[d] - m->blk.origin[d]);
+      off += m->blk.origin[d] * os[d];
+    }
+    inr_status s = inr_decode_grid_part(m, res, cnt, grid + off, os, nullptr, nullptr, st);
+    if (s) return s;
+  }
+  return INR_OK;
+}
+
+extern "C" inr_status inr_pathlines(const inr_cache* c, int32_t window_ops, const double* seeds, int32_t nseeds,
+                                    double dt, int32_t max_steps, double* vertices, int32_t* counts,
+                                    int32_t* reasons, cudaStream_t st) {
+  if (!c) return fail(INR_ERR_INVALID_ARG, "cache is NULL");
+  if (c->slots.size() < 2) return fail(INR_ERR_INVALID_ARG, "a pathline window needs at least two timesteps");
+  inr_status s = check_path_args(seeds, nseeds, dt, max_steps, vertices, counts, reasons);
+  if (s) return s;
+  if (nseeds == 0) return INR_OK;
+  const int W = (int)c->slots.size();
+  const inr_model* m0 = c->slots[0].cmodels[0];
+  const int64_t N[3] = {m0->blk.global_dims[0], m0->blk.global_dims[1], m0->blk.global_dims[2]};
+  const long long n[3] = {N[0], N[1], N[2]};
+  const bool rev = window_ops & INR_WINDOW_REVERSE;
+  const double sign = (window_ops & INR_WINDOW_NEGATE) ? -1.0 : 1.0;
+  // element i of the (reversed) window and its time (tau_i = t_last - t_{W-1-i} when reversed)
+  auto elem = [&](int i) -> const CacheSlot& { return c->slots[rev ? W - 1 - i : i]; };
+  auto time = [&](int i) -> double {
+    return rev ? (double)c->slots[W - 1].timestep - (double)c->slots[W - 1 - i].timestep
+               : (double)c->slots[i].timestep;
+  };
+  CK(cudaSetDevice(c->device));
+  keep_pool(c->device);
+  float* buf[2] = {nullptr, nullptr};
+  const size_t bytes = (size_t)N[0] * N[1] * N[2] * 3 * sizeof(float);
+  CK(cudaMallocAsync((void**)&buf[0], bytes, st));
+  CK(cudaMallocAsync((void**)&buf[1], bytes, st));
+  struct Free {
+    float** b; cudaStream_t s;
+    ~Free() { cudaFreeAsync(b[0], s); cudaFreeAsync(b[1], s); }
+  } release{buf, st};
+  // two grids resident: element i + 1 is decoded into the buffer element i - 1 held
+  s = decode_element(elem(0), buf[0], N, st);
+  if (s) return s;
+  s = decode_element(elem(1), buf[1], N, st);
+  if (s) return s;
+  {
+    ProfScope p(PK_PATHLINE, st);
+    launch_path_init(buf[0], buf[1], n, time(0), sign, seeds, nseeds, max_steps, vertices, counts, reasons, st);
+  }
+  for (int i = 0; i + 1 < W; ++i) {
+    if (i > 0) {
+      s = decode_element(elem(i + 1), buf[(i + 1) & 1], N, st);
+      if (s) return s;
+    }
+    ProfScope p(PK_PATHLINE, st);
+    launch_path_interval(buf[i & 1], buf[(i + 1) & 1], n, time(i), time(i + 1), dt, sign, max_steps, nseeds,
+                         vertices, counts, reasons, st);
+  }
+  {
+    ProfScope p(PK_PATHLINE, st);
+    launch_path_finish(nseeds, reasons, st);
+  }
+  CK_LAUNCH("pathlines");
+  return INR_OK;
+}
+

@@ -285,21 +285,22 @@ __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
 // in normalized units against ref (R18).
 template <int F>
 __global__ void __launch_bounds__(kTile) decode_grid_simt_kernel(NetDesc net, ModelDev md, int rx, int ry, int rz,
+                                                                 int cx, int cy, int cz,
                                                                  float* __restrict__ out, long long os0,
                                                                  long long os1, long long os2,
                                                                  const float* __restrict__ ref,
                                                                  double* __restrict__ sse) {
   extern __shared__ float smem[];
   const int t = threadIdx.x;
-  const long long total = (long long)rx * ry * rz;
+  const long long total = (long long)cx * cy * cz;   // the first c_d of the R_d lattice points per axis
   const long long j = blockIdx.x * (long long)kTile + t;
   const bool valid = j < total;
   int jx = 0, jy = 0, jz = 0;
   if (valid) {
-    jx = (int)(j % rx);
-    long long r = j / rx;
-    jy = (int)(r % ry);
-    jz = (int)(r / ry);
+    jx = (int)(j % cx);
+    long long r = j / cx;
+    jy = (int)(r % cy);
+    jz = (int)(r / cy);
   }
   float x[3] = {__fdiv_rn((float)jx, (float)rx), __fdiv_rn((float)jy, (float)ry), __fdiv_rn((float)jz, (float)rz)};
   encode_to_smem<F>(net, md.params, x, smem, t);
@@ -517,14 +518,14 @@ void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st) {
   count_launch();
 }
 
-void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                              const long long os[3], const float* ref, double* sse, cudaStream_t st) {
-  long long total = (long long)res[0] * res[1] * res[2];
+  long long total = (long long)cnt[0] * cnt[1] * cnt[2];
   size_t sm = simt_fwd_smem(net);
   unsigned grid = (unsigned)((total + kTile - 1) / kTile);
   DISPATCH_F(net.F, set_smem(decode_grid_simt_kernel<FF>, sm);
-             decode_grid_simt_kernel<FF><<<grid, kTile, sm, st>>>(net, md, res[0], res[1], res[2], out, os[0], os[1],
-                                                                  os[2], ref, sse));
+             decode_grid_simt_kernel<FF><<<grid, kTile, sm, st>>>(net, md, res[0], res[1], res[2], cnt[0], cnt[1],
+                                                                  cnt[2], out, os[0], os[1], os[2], ref, sse));
   count_launch();
 }
 

@@ -526,7 +526,7 @@ struct FwdArgs {
   const float* x01;
   float* y;
   long long q;
-  int res[3];
+  int res[3], cnt[3];   // decode grid: lattice resolution, points decoded per axis (cnt <= res)
   float* out;
   long long os[3];
   const float* ref;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   // a CTA reloads weights only when its next tile belongs to another block
   long long ntiles;
   if constexpr (MODE == 0) ntiles = (a.q + kTileM - 1) / kTileM;
-  else if constexpr (MODE == 1) ntiles = ((long long)a.res[0] * a.res[1] * a.res[2] + kTileM - 1) / kTileM;
+  else if constexpr (MODE == 1) ntiles = ((long long)a.cnt[0] * a.cnt[1] * a.cnt[2] + kTileM - 1) / kTileM;
   else ntiles = *a.ntiles_dev;
   const long long t0 = blockIdx.x, t1 = ntiles, tstep = gridDim.x;
   for (long long tile = t0; tile < t1; tile += tstep) {
@@ -596,11 +596,11 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
       valid = j < a.q;
       if (valid) { x[0] = __ldg(a.x01 + 3 * j); x[1] = __ldg(a.x01 + 3 * j + 1); x[2] = __ldg(a.x01 + 3 * j + 2); }
     } else if constexpr (MODE == 1) {
-      valid = j < (long long)a.res[0] * a.res[1] * a.res[2];
+      valid = j < (long long)a.cnt[0] * a.cnt[1] * a.cnt[2];
       if (valid) {
-        const int jx = (int)(j % a.res[0]);
-        const long long r = j / a.res[0];
-        const int jy = (int)(r % a.res[1]), jz = (int)(r / a.res[1]);
+        const int jx = (int)(j % a.cnt[0]);
+        const long long r = j / a.cnt[0];
+        const int jy = (int)(r % a.cnt[1]), jz = (int)(r / a.cnt[1]);
         x[0] = __fdiv_rn((float)jx, (float)a.res[0]);
         x[1] = __fdiv_rn((float)jy, (float)a.res[1]);
         x[2] = __fdiv_rn((float)jz, (float)a.res[2]);
@@ -754,15 +754,15 @@ void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x0
   launch_forward<0>(*single_group(net, md), a, (q + kTileM - 1) / kTileM, st);
 }
 
-void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                            const long long os[3], const float* ref, double* sse, cudaStream_t st) {
   FwdArgs a;
   memset(&a, 0, sizeof a);
-  for (int d = 0; d < 3; ++d) { a.res[d] = res[d]; a.os[d] = os[d]; }
+  for (int d = 0; d < 3; ++d) { a.res[d] = res[d]; a.cnt[d] = cnt[d]; a.os[d] = os[d]; }
   a.out = out;
   a.ref = ref;
   a.sse = sse;
-  long long n = (long long)res[0] * res[1] * res[2];
+  long long n = (long long)cnt[0] * cnt[1] * cnt[2];
   launch_forward<1>(*single_group(net, md), a, (n + kTileM - 1) / kTileM, st);
 }
 

@@ -40,13 +40,21 @@ inline int qa_nmodels(const QueryArgs& qa) { return qa.nmodels; }
 
 void count_launch(long long n = 1);
 
+// pathlines (kernels_path.cu)
+void launch_path_init(const float* g0, const float* g1, const long long n[3], double t0, double sign,
+                      const double* seeds, int M, int max_steps, double* vert, int* count, int* reason,
+                      cudaStream_t st);
+void launch_path_interval(const float* g0, const float* g1, const long long n[3], double ta, double tb, double dt,
+                          double sign, int max_steps, int M, double* vert, int* count, int* reason, cudaStream_t st);
+void launch_path_finish(int M, int* reason, cudaStream_t st);
+
 void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t k1, uint32_t block_id,
                         cudaStream_t st);
 void launch_step_begin(const GroupArgs& g, int nmodels, long long zero_from, cudaStream_t st);
 void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
 void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st);
 void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st);
-void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                              const long long os[3], const float* ref, double* sse, cudaStream_t st);
 void launch_decode_query_simt(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag,
                               cudaStream_t st);
@@ -91,7 +99,7 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
                    const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st);
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
-void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], float* out,
+void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                            const long long os[3], const float* ref, double* sse, cudaStream_t st);
 void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const int* perm,
                             const int* tile_slot, const int* ntiles_dev, cudaStream_t st);

@@ -222,12 +222,13 @@ class DNR:
         for b, m in zip(self.block_ids, self.models):
             o = block_origin(b, self.global_dims, self.n)
             off = [(o[d] - self.lo[d]) * scale for d in range(3)]
-            # a block at the upper domain face decodes the lattice points up to N (R19)
-            r = tuple(min(res[d], (self.global_dims[d] - o[d]) * scale) for d in range(3))
+            # a block at the upper domain face decodes only the lattice points up to N (R19):
+            # the first (N - o) * scale points of its res-point lattice
+            cnt = tuple(min(res[d], (self.global_dims[d] - o[d]) * scale) for d in range(3))
             base = out[off[2]:, off[1]:, off[0]:]
             refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
-            self.inr.inr_decode_grid(m, r, base.data_ptr(), self._strides(nx, ny), refp,
-                                     sse.data_ptr() if sse is not None else None, stream)
+            self.inr.inr_decode_grid(m, res, base.data_ptr(), self._strides(nx, ny), refp,
+                                     sse.data_ptr() if sse is not None else None, stream, count=cnt)
 
     def core_box(self):
         """(lo, hi inclusive) of this rank's core nodes (the ghost layer excluded)."""

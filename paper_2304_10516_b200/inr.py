@@ -94,6 +94,8 @@ _SIG = {
     "inr_decode": (_I32, [_P, _P, _I64, _P, _I32, _P]),
     "inr_decode_group": (_I32, [_PP, _I32, _P, _I64, _P, _I32, _P]),
     "inr_decode_grid": (_I32, [_P, ctypes.POINTER(_I32), _P, ctypes.POINTER(_I64), _P, _P, _P]),
+    "inr_decode_grid_part": (_I32, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), _P, ctypes.POINTER(_I64), _P,
+                                    _P, _P]),
     "inr_value_range": (_I32, [ctypes.POINTER(inr_view), _P, _P]),
     "cache_create": (_I32, [_I32, _I32, ctypes.c_int, _PP]),
     "cache_destroy": (_I32, [_P]),
@@ -102,6 +104,10 @@ _SIG = {
     "cache_size": (_I32, [_P, ctypes.POINTER(_I32)]),
     "cache_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
     "cache_get": (_I32, [_P, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_PP), ctypes.POINTER(_I32)]),
+    "inr_trace_grids": (_I32, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_double), _I32,
+                               ctypes.POINTER(_I64), ctypes.c_double, _P, _I32, ctypes.c_double, _I32, _P, _P, _P,
+                               _P]),
+    "inr_pathlines": (_I32, [_P, _I32, _P, _I32, ctypes.c_double, _I32, _P, _P, _P, _P]),
     "inr_get_params": (_I32, [_P, _P, _I64]),
     "inr_set_params": (_I32, [_P, _P, _I64]),
     "inr_get_grads": (_I32, [_P, _P, _I64]),
@@ -217,14 +223,35 @@ def inr_decode_group(models, xyz_ptr, q, out_ptr, strict=0, stream=0):
     _check(_lib.inr_decode_group(pp, len(models), xyz_ptr, q, out_ptr, strict, stream))
 
 
-def inr_decode_grid(m, res, out_ptr, out_stride=None, ref_ptr=None, sse_ptr=None, stream=0):
+def inr_decode_grid(m, res, out_ptr, out_stride=None, ref_ptr=None, sse_ptr=None, stream=0, count=None):
     r = (_I32 * 3)(*res)
     s = (_I64 * 3)(*out_stride) if out_stride is not None else None
-    _check(_lib.inr_decode_grid(m, r, out_ptr, s, ref_ptr, sse_ptr, stream))
+    if count is None:
+        _check(_lib.inr_decode_grid(m, r, out_ptr, s, ref_ptr, sse_ptr, stream))
+    else:
+        _check(_lib.inr_decode_grid_part(m, r, (_I32 * 3)(*count), out_ptr, s, ref_ptr, sse_ptr, stream))
 
 
 def inr_value_range(view, minmax_ptr, stream=0):
     _check(_lib.inr_value_range(ctypes.byref(view), minmax_ptr, stream))
+
+
+# ---- pathlines (NEXT-2)
+INR_PATH_WINDOW_EXHAUSTED, INR_PATH_OUT_OF_DOMAIN, INR_PATH_MAX_STEPS = 0, 1, 2
+INR_WINDOW_REVERSE, INR_WINDOW_NEGATE = 1, 2
+
+
+def inr_trace_grids(grid_ptrs, times, dims, sign, seeds_ptr, nseeds, dt, max_steps, vert_ptr, counts_ptr,
+                    reasons_ptr, stream=0):
+    g = (ctypes.c_void_p * len(grid_ptrs))(*grid_ptrs)
+    t = (ctypes.c_double * len(times))(*[float(v) for v in times])
+    _check(_lib.inr_trace_grids(ctypes.cast(g, _PP), t, len(grid_ptrs), (_I64 * 3)(*dims), float(sign), seeds_ptr,
+                                nseeds, float(dt), max_steps, vert_ptr, counts_ptr, reasons_ptr, stream))
+
+
+def inr_pathlines(cache, window_ops, seeds_ptr, nseeds, dt, max_steps, vert_ptr, counts_ptr, reasons_ptr, stream=0):
+    _check(_lib.inr_pathlines(cache, window_ops, seeds_ptr, nseeds, float(dt), max_steps, vert_ptr, counts_ptr,
+                              reasons_ptr, stream))
 
 
 # ---- cache
