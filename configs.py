@@ -281,6 +281,115 @@ def run_cfg5(stream, prec):
     return r
 
 
+def run_next2(stream, prec, n=256, window=10, steps=500, M=1 << 16, dt=0.1, amp=2.0):
+    """NEXT-2: a time-varying Taylor-Green velocity field (G4, 256^3,
+    8 blocks of 128^3, D = 3) fitted per timestep (500 steps) into a window of 10;
+    then backward pathlines P = pathline(negate(reverse(W))) of M seeds
+    from a box, the forward pass from their end points (Fig. 8A round trip), and
+    the same backward trace on the ground-truth grids (Fig. 8B comparison)."""
+    dev = torch.device("cuda")
+    gd = (n, n, n)
+    cfg = inr.make_config(precision=prec, out_dim=3, **NET2)
+    d = dnr.DNR(gd, (128, 128, 128), cfg)
+    cache = inr.cache_create(window + 1, 0, 0)
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = 16384
+    lat = synth.lattice(gd, dev)
+    gt, fit_ms, psnrs = [], [], []
+    for ts in range(window):
+        vol = synth.taylor_green(lat, gd, float(ts), amp=amp).to(torch.float32).contiguous()
+        d.value_range(vol, stream)
+        for m in d.models:
+            inr.inr_reset(m, 0x230410516 + ts)
+        e0, e1 = ev(), ev()
+        e0.record()
+        d.fit(vol, steps, 65536, opts, stream, report=True)
+        e1.record()
+        torch.cuda.synchronize()
+        fit_ms.append(e0.elapsed_time(e1))
+        out = torch.empty_like(vol)
+        sse = torch.zeros(1, dtype=torch.float64, device=dev)
+        d.decode_grid_local(out, 1, vol, sse, stream)
+        torch.cuda.synchronize()
+        psnrs.append(d.psnr(float(sse.item()), 3 * n ** 3))
+        inr.cache_insert(cache, ts, d.models, stream)
+        gt.append(vol)
+        del out
+    del lat
+    rng = np.random.default_rng(11)
+    lo_box, hi_box = np.array([64.0, 64.0, 64.0]), np.array([192.0, 192.0, 192.0])
+    seeds = lo_box + rng.random((M, 3)) * (hi_box - lo_box)
+    K = int(math.ceil((window - 1) / dt)) + 2
+
+    def run(fn):
+        vert = torch.empty((M, K + 1, 5), dtype=torch.float64, device=dev)
+        cnt = torch.empty(M, dtype=torch.int32, device=dev)
+        why = torch.empty(M, dtype=torch.int32, device=dev)
+        fn(vert, cnt, why)               # warm
+        torch.cuda.synchronize()
+        inr.inr_profile_enable(1)
+        e0, e1 = ev(), ev()
+        e0.record()
+        fn(vert, cnt, why)
+        e1.record()
+        torch.cuda.synchronize()
+        kms = inr.inr_profile_read("pathline")[0]
+        inr.inr_profile_enable(0)
+        return vert, cnt, why, e0.elapsed_time(e1), kms
+
+    sd = torch.from_numpy(seeds).to(dev)
+    ops = inr.INR_WINDOW_REVERSE | inr.INR_WINDOW_NEGATE
+    vb, cb, rb, ms_b, kms_b = run(lambda v, c, w: inr.inr_pathlines(cache, ops, sd.data_ptr(), M, dt, K, v.data_ptr(),
+                                                                    c.data_ptr(), w.data_ptr(), stream))
+    cbn, rbn = cb.cpu().numpy(), rb.cpu().numpy()
+    ok = rbn == inr.INR_PATH_WINDOW_EXHAUSTED
+    ends = vb[torch.arange(M, device=dev), cb.long() - 1, :3].contiguous()
+    steps_b = int((cbn - 1).clip(min=0).sum())
+    # forward from the backward end points (Fig. 8A): seeds that left the domain are dropped (P:L434)
+    ok_t = torch.from_numpy(ok).to(dev)
+    ends_ok = ends[ok_t].contiguous()
+    Mf = int(ends_ok.shape[0])
+    vf = torch.empty((Mf, K + 1, 5), dtype=torch.float64, device=dev)
+    cf = torch.empty(Mf, dtype=torch.int32, device=dev)
+    rf = torch.empty(Mf, dtype=torch.int32, device=dev)
+    inr.inr_pathlines(cache, 0, ends_ok.data_ptr(), Mf, dt, K, vf.data_ptr(), cf.data_ptr(), rf.data_ptr(), stream)
+    torch.cuda.synchronize()
+    back = vf[torch.arange(Mf, device=dev), cf.long() - 1, :3]
+    fin = rf == inr.INR_PATH_WINDOW_EXHAUSTED
+    rt = (back - sd[ok_t])[fin].norm(dim=1).cpu().numpy()
+    # ground truth: the same backward trace on the analytic grids (post hoc, P:L428)
+    times = [float(t) for t in range(window)]
+    gt_rev = gt[::-1]
+    tau = [times[-1] - t for t in times[::-1]]
+    vg, cg, rg, ms_g, _ = run(lambda v, c, w: inr.inr_trace_grids([g.data_ptr() for g in gt_rev], tau, gd, -1.0,
+                                                                   sd.data_ptr(), M, dt, K, v.data_ptr(),
+                                                                   c.data_ptr(), w.data_ptr(), stream))
+    both = ok & (rg.cpu().numpy() == inr.INR_PATH_WINDOW_EXHAUSTED)
+    bt = torch.from_numpy(both).to(dev)
+    gends = vg[torch.arange(M, device=dev), cg.long() - 1, :3]
+    dev_gt = (ends - gends)[bt].norm(dim=1).cpu().numpy()
+    r = {"config": "NEXT-2 Taylor-Green 256^3 (8 x 128^3 blocks, D=3), window 10, backward pathlines",
+         "precision": "fp16" if prec else "fp32", "fit_steps_per_timestep": steps,
+         "fit_coords_per_s": 8 * (65536 + 16384) * steps / (np.mean(fit_ms) / 1e3),
+         "psnr_db_mean": float(np.mean(psnrs)), "psnr_db_min": float(np.min(psnrs)),
+         "compression_ratio": 3 * 4.0 * n ** 3 / d.param_bytes(),
+         "seeds": M, "dt": dt, "substeps_per_seed_max": K,
+         "backward_ms_total": ms_b, "backward_ms_kernels": kms_b,
+         "backward_ms_decode": ms_b - kms_b,
+         "particle_steps": steps_b, "particle_steps_per_s_kernels": steps_b / (kms_b / 1e3),
+         "particle_steps_per_s_with_decode": steps_b / (ms_b / 1e3),
+         "seeds_exhausted_window": int(ok.sum()), "seeds_left_domain": int((rbn == 1).sum()),
+         "roundtrip_err_nodes": {"median": float(np.median(rt)), "p99": float(np.percentile(rt, 99)),
+                                 "max": float(rt.max()), "n": int(rt.size)},
+         "dnr_vs_ground_truth_endpoint_nodes": {"median": float(np.median(dev_gt)),
+                                                "p90": float(np.percentile(dev_gt, 90)),
+                                                "max": float(dev_gt.max()), "n": int(dev_gt.size)},
+         "ground_truth_trace_ms": ms_g}
+    inr.cache_destroy(cache)
+    d.close()
+    return r
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="cfg1,cfg2,cfg2r,cfg3,cfg4,cfg5")
@@ -290,12 +399,12 @@ def main():
     torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
     fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg2r": run_cfg2r, "cfg3": run_cfg3, "cfg4": run_cfg4,
-           "cfg5": run_cfg5}
+           "cfg5": run_cfg5, "next2": run_next2}
     results = []
     for name in a.only.split(","):
         for p in a.precision.split(","):
             prec = inr.INR_PREC_FP16_MLP if p == "fp16" else inr.INR_PREC_FP32
-            if name in ("cfg2r", "cfg3", "cfg4", "cfg5") and p == "fp32":
+            if name in ("cfg2r", "cfg3", "cfg4", "cfg5", "next2") and p == "fp32":
                 continue          # the fp32 CUDA-core path is the parity mode; large configs run fp16
             t0 = time.time()
             r = fns[name](stream, prec)
