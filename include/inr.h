@@ -283,6 +283,58 @@ INR_API inr_status inr_pathlines(const inr_cache* c, int32_t window_ops, const d
                          double dt, int32_t max_steps, double* vertices, int32_t* counts, int32_t* reasons,
                          cudaStream_t stream);
 
+/* ---- direct-query volume rendering (NEXT-3) ----
+ * Scalar-field (out_dim 1) models only.  World coordinates = global node
+ * coordinates.  The optical model and sampling are DESIGN.md R32-R35:
+ *   pixel (px, py), py = 0 the top row, ray eye + t d with d = normalize(f +
+ *   a r + b u), a = (2 (px + .5)/W - 1) tan(fovy/2) W/H, b = (1 - 2 (py + .5)/H)
+ *   tan(fovy/2), f = normalize(look - eye), r = normalize(f x up), u = r x f;
+ *   samples at t_k = (k + 0.5) step (global along the ray), a brick [lo, hi]
+ *   takes t_enter <= t_k < t_exit; value v = the DNR query at the fp32-rounded
+ *   position (routed as inr_decode_group); s = clamp((v - vmin)/(vmax - vmin));
+ *   RGBA = piecewise-linear transfer function; a = 1 - (1 - a_tf)^(step/base_step);
+ *   C += (1 - A) a c, A += (1 - A) a, stop when A >= stop_alpha. */
+#define INR_TF_MAX_POINTS 16
+typedef struct {
+  double eye[3], look[3], up[3];
+  double fovy_deg;
+  int32_t width, height;
+} inr_camera;
+typedef struct {
+  int32_t npoints;                       /* 2..INR_TF_MAX_POINTS, s strictly increasing in [0, 1] */
+  float s[INR_TF_MAX_POINTS];
+  float rgba[INR_TF_MAX_POINTS][4];      /* colour and opacity in [0, 1] */
+  double vmin, vmax;                     /* data values mapped to s = 0 and 1 */
+  double base_step;                      /* the step the opacities are defined for */
+} inr_transfer_fn;
+typedef struct inr_renderer inr_renderer;
+/* Bind nmodels (<= 64) models of one volume (one rank's blocks) and build the
+ * macro-cell grid: cells^3 cells per block, each cell's value range from a
+ * (4 cells)^3 probe lattice decoded per block (cells of an axis take their own
+ * probes and the neighbouring probe across each face), padded by pad (data
+ * units) ("macro-cell acceleration structure").  The models
+ * must outlive the renderer and stay frozen while it is used. */
+INR_API inr_status inr_renderer_create(const inr_model* const* models, int32_t nmodels, int32_t cells, double pad,
+                               cudaStream_t stream, inr_renderer** out);
+INR_API inr_status inr_renderer_destroy(inr_renderer* r);
+/* Ray-march the brick [brick_lo, brick_hi] (normally this rank's core box)
+ * by sample streaming: waves of up to 64 samples per live ray are generated
+ * (samples in macro-cells whose transfer-function opacity is 0 over their
+ * range are skipped when use_macrocells != 0), decoded with the tensor-core
+ * query path, and composited.  fragments (dev) [H*W][5] = (C_r, C_g, C_b, A,
+ * t_enter), t_enter = +inf for rays that miss the brick.  Synchronizes stream
+ * once per wave. */
+INR_API inr_status inr_render(inr_renderer* r, const inr_camera* cam, const inr_transfer_fn* tf,
+                      const double brick_lo[3], const double brick_hi[3], double step, double stop_alpha,
+                      int32_t use_macrocells, float* fragments, cudaStream_t stream);
+/* Samples evaluated / skipped and waves of the last inr_render. */
+INR_API inr_status inr_render_stats(const inr_renderer* r, int64_t* evaluated, int64_t* skipped, int32_t* waves);
+/* Sort-last compositing: fragments (dev) [nfrag][npixels][5] from
+ * nfrag <= 64 bricks, front to back by t_enter per pixel, then the background
+ * bg (host RGB): image (dev) [npixels][4] RGBA. */
+INR_API inr_status inr_composite(const float* fragments, int32_t nfrag, int64_t npixels, const float bg[3],
+                         float* image, cudaStream_t stream);
+
 /* ---- parity / test surface ---- */
 /* Copy n = inr_param_count floats of parameters / last-step gradients / Adam m /
  * Adam v in the declared order (synchronous). */

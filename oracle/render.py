@@ -72,44 +72,71 @@ def tf_lookup(s, points, rgba):
     return np.array([np.interp(s, points, rgba[:, c]) for c in range(4)])
 
 
-def ray_segment(field, eye, d, t_enter, t_exit, step, tf, stop_alpha=0.99):
-    """Front-to-back emission-absorption over the samples of [t_enter, t_exit)
-    (S:L468-476).  field(p (3,)) -> value.  Returns (C (3,), A)."""
-    C = np.zeros(3)
-    A = 0.0
+def sample_ts(t_enter, t_exit, step):
+    """The global sample parameters t_k = (k + 0.5) step in [t_enter, t_exit)."""
     if not t_exit > t_enter:
-        return C, A
+        return np.zeros(0)
     k = max(0, math.ceil(t_enter / step - 0.5) - 1)   # one early: the t >= t_enter test decides
+    ts = []
     while True:
         t = (k + 0.5) * step
         if t >= t_exit:
             break
         if t >= t_enter:
-            v = field(eye + t * d)
-            s = min(max((v - tf["vmin"]) / (tf["vmax"] - tf["vmin"]), 0.0), 1.0)
-            r, g, b, a_tf = tf_lookup(s, tf["points"], tf["rgba"])
-            a = 1.0 - (1.0 - a_tf) ** (step / tf["base_step"])
-            w = (1.0 - A) * a
-            C = C + w * np.array([r, g, b])
-            A = A + w
-            if A >= stop_alpha:
-                break
+            ts.append(t)
         k += 1
+    return np.array(ts)
+
+
+def march(values, step, tf, stop_alpha=0.99):
+    """Front-to-back emission-absorption over the sample values in ray order
+    (S:L468-476).  Returns (C (3,), A)."""
+    C = np.zeros(3)
+    A = 0.0
+    for v in values:
+        s = min(max((v - tf["vmin"]) / (tf["vmax"] - tf["vmin"]), 0.0), 1.0)
+        r, g, b, a_tf = tf_lookup(s, tf["points"], tf["rgba"])
+        a = 1.0 - (1.0 - a_tf) ** (step / tf["base_step"])
+        w = (1.0 - A) * a
+        C = C + w * np.array([r, g, b])
+        A = A + w
+        if A >= stop_alpha:
+            break
     return C, A
 
 
-def render_brick(field, cam, lo, hi, step, tf, stop_alpha=0.99):
+def ray_segment(field, eye, d, t_enter, t_exit, step, tf, stop_alpha=0.99):
+    """One ray through one brick; field(p (3,)) -> value.  Returns (C, A)."""
+    ts = sample_ts(t_enter, t_exit, step)
+    return march([field(eye + t * d) for t in ts], step, tf, stop_alpha)
+
+
+def render_brick(field, cam, lo, hi, step, tf, stop_alpha=0.99, batch_field=None):
     """Fragments of one brick: (H*W, 5) rows (C_r, C_g, C_b, A, t_enter);
-    t_enter = +inf where the ray misses the brick."""
+    t_enter = +inf where the ray misses the brick.  batch_field(P (n, 3))
+    evaluates all sample positions at once instead of field (same values: the
+    samples after an early stop are computed but not composited)."""
     eye = np.asarray(cam["eye"], np.float64)
     dirs = camera_rays(cam["eye"], cam["look"], cam["up"], cam["fovy"], cam["width"], cam["height"])
     out = np.zeros((dirs.shape[0], 5))
+    segs = []
     for i, d in enumerate(dirs):
         t0, t1 = box_interval(eye, d, lo, hi)
+        segs.append((t0, t1, sample_ts(t0, t1, step)))
+    if batch_field is not None:
+        pts = [eye[None, :] + ts[:, None] * d[None, :] for (_, _, ts), d in zip(segs, dirs)]
+        allv = batch_field(np.concatenate(pts)) if sum(p.shape[0] for p in pts) else np.zeros(0)
+        offs = np.cumsum([0] + [p.shape[0] for p in pts])
+    for i, d in enumerate(dirs):
+        t0, t1, ts = segs[i]
         if not t1 > t0:
             out[i, 4] = math.inf
             continue
-        C, A = ray_segment(field, eye, d, t0, t1, step, tf, stop_alpha)
+        if batch_field is not None:
+            vals = allv[offs[i]:offs[i + 1]]
+        else:
+            vals = [field(eye + t * d) for t in ts]
+        C, A = march(vals, step, tf, stop_alpha)
         out[i, :3], out[i, 3], out[i, 4] = C, A, t0
     return out
 

@@ -1186,3 +1186,228 @@ extern "C" inr_status inr_pathlines(const inr_cache* c, int32_t window_ops, cons
   return INR_OK;
 }
 
+
+// ------------------------------------------------------------------ rendering
+// NEXT-3: direct-query DVR of one rank's
+// blocks by sample streaming, macro-cell skipping, sort-last compositing.
+struct inr_renderer {
+  int device = 0;
+  std::vector<const inr_model*> models;
+  int cells = 16;
+  int n[3], B[3];
+  int* slot_of_block = nullptr;   // device [nblocks]
+  float2* range = nullptr;        // device [nmodels][cells^3] (data units, padded)
+  uint8_t* empty = nullptr;       // device [nmodels][cells^3]
+  int64_t evaluated = 0, skipped = 0;
+  int waves = 0;
+};
+
+extern "C" inr_status inr_renderer_destroy(inr_renderer* r) {
+  if (!r) return INR_OK;
+  cudaSetDevice(r->device);
+  cudaFree(r->slot_of_block);
+  cudaFree(r->range);
+  cudaFree(r->empty);
+  delete r;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_renderer_create(const inr_model* const* models, int32_t nmodels, int32_t cells, double pad,
+                                          cudaStream_t st, inr_renderer** out) {
+  if (!out) return fail(INR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!models || nmodels < 1) return fail(INR_ERR_INVALID_ARG, "models missing");
+  if (nmodels > kMaxGroup) return fail(INR_ERR_UNSUPPORTED, "at most %d models per renderer", kMaxGroup);
+  if (cells < 1 || cells > 64) return fail(INR_ERR_INVALID_ARG, "cells must be in 1..64");
+  if (!(pad >= 0.0)) return fail(INR_ERR_INVALID_ARG, "pad must be >= 0");
+  const inr_model* m0 = models[0];
+  if (!m0) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
+  if (m0->net.D != 1) return fail(INR_ERR_UNSUPPORTED, "volume rendering needs scalar-field (out_dim 1) models");
+  long long nb = 1;
+  int n[3], B[3];
+  for (int d = 0; d < 3; ++d) {
+    n[d] = m0->blk.n[d];
+    B[d] = (int)((m0->blk.global_dims[d] + n[d] - 1) / n[d]);
+    nb *= B[d];
+  }
+  if (nb > kMaxRouteBlocks) return fail(INR_ERR_UNSUPPORTED, "at most %d blocks in a volume", kMaxRouteBlocks);
+  std::vector<int> sob((size_t)nb, -1);
+  for (int i = 0; i < nmodels; ++i) {
+    const inr_model* m = models[i];
+    if (!m || !same_shape(m->cfg, m0->cfg) || m->device != m0->device)
+      return fail(INR_ERR_INVALID_ARG, "renderer models must share config and device");
+    for (int d = 0; d < 3; ++d)
+      if (m->blk.n[d] != n[d] || m->blk.global_dims[d] != m0->blk.global_dims[d])
+        return fail(INR_ERR_INVALID_ARG, "renderer models must tile one volume");
+    sob[m->block_id] = i;
+  }
+  CK(cudaSetDevice(m0->device));
+  keep_pool(m0->device);
+  inr_renderer* r = new inr_renderer();
+  r->device = m0->device;
+  r->models.assign(models, models + nmodels);
+  r->cells = cells;
+  for (int d = 0; d < 3; ++d) { r->n[d] = n[d]; r->B[d] = B[d]; }
+  const long long nc = (long long)nmodels * cells * cells * cells;
+  if (cudaMalloc((void**)&r->slot_of_block, sizeof(int) * nb) != cudaSuccess ||
+      cudaMalloc((void**)&r->range, sizeof(float2) * nc) != cudaSuccess ||
+      cudaMalloc((void**)&r->empty, nc) != cudaSuccess) {
+    inr_renderer_destroy(r);
+    return fail(INR_ERR_OOM, "renderer allocation");
+  }
+  CK(cudaMemcpyAsync(r->slot_of_block, sob.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  // probe lattice per block: R = 4 cells per axis, decoded on the library's grid path
+  const int P = 4, R = cells * P;
+  float* probes = nullptr;
+  CK(cudaMallocAsync((void**)&probes, sizeof(float) * (size_t)nmodels * R * R * R, st));
+  const int32_t res[3] = {R, R, R};
+  for (int i = 0; i < nmodels; ++i) {
+    inr_status s = inr_decode_grid(models[i], res, probes + (size_t)i * R * R * R, nullptr, nullptr, nullptr, st);
+    if (s) { cudaFreeAsync(probes, st); inr_renderer_destroy(r); return s; }
+  }
+  launch_mc_reduce(probes, nmodels, cells, P, (float)pad, r->range, st);
+  CK_LAUNCH("macro-cells");
+  CK(cudaFreeAsync(probes, st));
+  *out = r;
+  return INR_OK;
+}
+
+static inr_status render_tf(const inr_transfer_fn* tf, RenderTF& t) {
+  if (!tf) return fail(INR_ERR_INVALID_ARG, "transfer function is NULL");
+  if (tf->npoints < 2 || tf->npoints > kTfMaxPoints)
+    return fail(INR_ERR_INVALID_ARG, "transfer function needs 2..%d points", kTfMaxPoints);
+  if (!(tf->vmax > tf->vmin)) return fail(INR_ERR_INVALID_ARG, "transfer function vmax must exceed vmin");
+  if (!(tf->base_step > 0.0)) return fail(INR_ERR_INVALID_ARG, "base_step must be > 0");
+  memset(&t, 0, sizeof t);
+  t.n = tf->npoints;
+  for (int i = 0; i < tf->npoints; ++i) {
+    if (i > 0 && !(tf->s[i] > tf->s[i - 1])) return fail(INR_ERR_INVALID_ARG, "transfer function s must increase");
+    t.s[i] = tf->s[i];
+    for (int c = 0; c < 4; ++c) {
+      if (!(tf->rgba[i][c] >= 0.f && tf->rgba[i][c] <= 1.f)) return fail(INR_ERR_INVALID_ARG, "rgba outside [0, 1]");
+      t.rgba[i][c] = tf->rgba[i][c];
+    }
+  }
+  t.vmin = (float)tf->vmin;
+  t.inv_range = (float)(1.0 / (tf->vmax - tf->vmin));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_render(inr_renderer* r, const inr_camera* cam, const inr_transfer_fn* tf,
+                                 const double lo[3], const double hi[3], double step, double stop_alpha,
+                                 int32_t use_mc, float* frag, cudaStream_t st) {
+  if (!r || !cam || !lo || !hi || !frag) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (cam->width < 1 || cam->height < 1 || (long long)cam->width * cam->height > (1ll << 28))
+    return fail(INR_ERR_INVALID_ARG, "image size");
+  if (!(cam->fovy_deg > 0.0 && cam->fovy_deg < 180.0)) return fail(INR_ERR_INVALID_ARG, "fovy must be in (0, 180)");
+  if (!(step > 0.0)) return fail(INR_ERR_INVALID_ARG, "step must be > 0");
+  RenderArgs a;
+  memset(&a, 0, sizeof a);
+  inr_status s = render_tf(tf, a.tf);
+  if (s) return s;
+  // camera basis (R33): f = normalize(look - eye), r = normalize(f x up), u = r x f
+  double f[3], rr[3], u[3];
+  for (int c = 0; c < 3; ++c) f[c] = cam->look[c] - cam->eye[c];
+  double nf = std::sqrt(f[0] * f[0] + f[1] * f[1] + f[2] * f[2]);
+  if (!(nf > 0.0)) return fail(INR_ERR_INVALID_ARG, "eye == look");
+  for (int c = 0; c < 3; ++c) f[c] /= nf;
+  rr[0] = f[1] * cam->up[2] - f[2] * cam->up[1];
+  rr[1] = f[2] * cam->up[0] - f[0] * cam->up[2];
+  rr[2] = f[0] * cam->up[1] - f[1] * cam->up[0];
+  double nr = std::sqrt(rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2]);
+  if (!(nr > 0.0)) return fail(INR_ERR_INVALID_ARG, "up is parallel to the view direction");
+  for (int c = 0; c < 3; ++c) rr[c] /= nr;
+  u[0] = rr[1] * f[2] - rr[2] * f[1];
+  u[1] = rr[2] * f[0] - rr[0] * f[2];
+  u[2] = rr[0] * f[1] - rr[1] * f[0];
+  for (int c = 0; c < 3; ++c) {
+    a.eye[c] = cam->eye[c]; a.f[c] = f[c]; a.r[c] = rr[c]; a.u[c] = u[c];
+    a.lo[c] = lo[c]; a.hi[c] = hi[c];
+    a.n[c] = r->n[c]; a.B[c] = r->B[c];
+  }
+  a.th = std::tan(cam->fovy_deg * M_PI / 180.0 / 2.0);
+  a.width = cam->width;
+  a.height = cam->height;
+  a.npix = cam->width * cam->height;
+  a.step = step;
+  a.exponent = (float)(step / tf->base_step);
+  a.stop_alpha = (float)stop_alpha;
+  a.cells = r->cells;
+  a.slot_of_block = r->slot_of_block;
+  CK(cudaSetDevice(r->device));
+  const int nm = (int)r->models.size();
+  const long long nc = (long long)nm * r->cells * r->cells * r->cells;
+  if (use_mc) {
+    launch_mc_mark(r->range, nc, a.tf, r->empty, st);
+    a.empty = r->empty;
+  }
+  const long long npix = a.npix;
+  const int S = (int)std::max<long long>(4, std::min<long long>(64, (1ll << 26) / npix));
+  // per-call workspace (stream-ordered): ray state, wave queries and values
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  const size_t o_dir = take(24 * npix), o_t0 = take(8 * npix), o_t1 = take(8 * npix), o_k = take(8 * npix),
+               o_live = take(4 * npix), o_C = take(16 * npix), o_base = take(4 * npix), o_nq = take(4 * npix),
+               o_q = take(12 * npix * S), o_v = take(4 * npix * S), o_cnt = take(16);
+  char* ws = nullptr;
+  CK(cudaMallocAsync((void**)&ws, off, st));
+  struct Free { char* p; cudaStream_t s; ~Free() { cudaFreeAsync(p, s); } } release{ws, st};
+  RayState rs;
+  rs.dir = (double*)(ws + o_dir);
+  rs.t_enter = (double*)(ws + o_t0);
+  rs.t_exit = (double*)(ws + o_t1);
+  rs.k = (long long*)(ws + o_k);
+  rs.live = (int*)(ws + o_live);
+  rs.C = (float*)(ws + o_C);
+  int* base = (int*)(ws + o_base);
+  int* nq = (int*)(ws + o_nq);
+  float* qxyz = (float*)(ws + o_q);
+  float* vals = (float*)(ws + o_v);
+  int* qcount = (int*)(ws + o_cnt);
+  unsigned long long* skipped = (unsigned long long*)(ws + o_cnt + 8);
+  CK(cudaMemsetAsync(ws + o_cnt, 0, 16, st));
+  r->evaluated = 0;
+  r->waves = 0;
+  launch_ray_init(a, rs, st);
+  for (;;) {
+    CK(cudaMemsetAsync(qcount, 0, sizeof(int), st));
+    launch_gen(a, rs, S, qxyz, qcount, base, nq, skipped, st);
+    CK_LAUNCH("render gen");
+    int q = 0;
+    CK(cudaMemcpyAsync(&q, qcount, sizeof q, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (q == 0) break;
+    s = decode_group_impl(r->models.data(), nm, qxyz, q, vals, 0, st);
+    if (s) return s;
+    launch_composite(a, rs, vals, base, nq, st);
+    CK_LAUNCH("render composite");
+    r->evaluated += q;
+    ++r->waves;
+  }
+  launch_fragments(a, rs, frag, st);
+  CK_LAUNCH("render fragments");
+  unsigned long long sk = 0;
+  CK(cudaMemcpyAsync(&sk, skipped, sizeof sk, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  r->skipped = (int64_t)sk;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_render_stats(const inr_renderer* r, int64_t* evaluated, int64_t* skipped, int32_t* waves) {
+  if (!r) return fail(INR_ERR_INVALID_ARG, "renderer is NULL");
+  if (evaluated) *evaluated = r->evaluated;
+  if (skipped) *skipped = r->skipped;
+  if (waves) *waves = r->waves;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_composite(const float* frags, int32_t nfrag, int64_t npix, const float bg[3], float* img,
+                                    cudaStream_t st) {
+  if (!frags || !img || !bg) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (nfrag < 1 || nfrag > kMaxFragments) return fail(INR_ERR_INVALID_ARG, "nfrag must be in 1..%d", kMaxFragments);
+  if (npix < 0) return fail(INR_ERR_INVALID_ARG, "npixels must be >= 0");
+  if (npix == 0) return INR_OK;
+  launch_blend(frags, nfrag, npix, bg, img, st);
+  CK_LAUNCH("composite");
+  return INR_OK;
+}

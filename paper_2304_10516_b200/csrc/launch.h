@@ -40,6 +40,44 @@ inline int qa_nmodels(const QueryArgs& qa) { return qa.nmodels; }
 
 void count_launch(long long n = 1);
 
+// volume rendering (kernels_render.cu, NEXT-3)
+constexpr int kTfMaxPoints = 16;
+constexpr int kMaxFragments = 64;
+struct RenderTF {
+  int n;
+  float s[kTfMaxPoints];
+  float rgba[kTfMaxPoints][4];
+  float vmin, inv_range;
+};
+struct RenderArgs {
+  double eye[3], f[3], r[3], u[3], th;   // camera: forward, right, up, tan(fovy / 2)
+  int width, height, npix;
+  double lo[3], hi[3];                   // the brick (global node coordinates)
+  double step;
+  float exponent, stop_alpha;            // step / base_step; early-termination opacity
+  RenderTF tf;
+  int n[3], B[3], cells;                 // block geometry (R5 routing) and macro-cells per block axis
+  const int* slot_of_block;              // [nblocks] slot or -1
+  const uint8_t* empty;                  // [slot][cells^3] 1 = no opacity for tf, or null (no skipping)
+};
+struct RayState {
+  double* dir;       // [npix][3]
+  double* t_enter;   // [npix]
+  double* t_exit;
+  long long* k;      // next sample index
+  int* live;
+  float* C;          // [npix][4] premultiplied RGB, A
+};
+void launch_mc_reduce(const float* probes, int nslots, int cells, int P, float pad, float2* range, cudaStream_t st);
+void launch_mc_mark(const float2* range, long long n, const RenderTF& tf, uint8_t* empty, cudaStream_t st);
+void launch_ray_init(const RenderArgs& a, const RayState& rs, cudaStream_t st);
+void launch_gen(const RenderArgs& a, const RayState& rs, int S, float* qxyz, int* qcount, int* base, int* nq,
+                unsigned long long* skipped, cudaStream_t st);
+void launch_composite(const RenderArgs& a, const RayState& rs, const float* vals, const int* base, const int* nq,
+                      cudaStream_t st);
+void launch_fragments(const RenderArgs& a, const RayState& rs, float* frag, cudaStream_t st);
+void launch_blend(const float* frags, int nfrag, long long npix, const float bg[3], float* img, cudaStream_t st);
+
 // pathlines (kernels_path.cu)
 void launch_path_init(const float* g0, const float* g1, const long long n[3], double t0, double sign,
                       const double* seeds, int M, int max_steps, double* vert, int* count, int* reason,

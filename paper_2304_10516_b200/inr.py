@@ -70,6 +70,32 @@ class inr_fit_report(ctypes.Structure):
                 ("loss_boundary", ctypes.c_double), ("probe_psnr", ctypes.c_double)]
 
 
+class inr_camera(ctypes.Structure):
+    _fields_ = [("eye", ctypes.c_double * 3), ("look", ctypes.c_double * 3), ("up", ctypes.c_double * 3),
+                ("fovy_deg", ctypes.c_double), ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class inr_transfer_fn(ctypes.Structure):
+    _fields_ = [("npoints", ctypes.c_int32), ("s", ctypes.c_float * 16), ("rgba", (ctypes.c_float * 4) * 16),
+                ("vmin", ctypes.c_double), ("vmax", ctypes.c_double), ("base_step", ctypes.c_double)]
+
+
+def make_camera(eye, look, up, fovy, width, height):
+    return inr_camera((ctypes.c_double * 3)(*eye), (ctypes.c_double * 3)(*look), (ctypes.c_double * 3)(*up),
+                      float(fovy), int(width), int(height))
+
+
+def make_tf(points, rgba, vmin, vmax, base_step=1.0):
+    t = inr_transfer_fn()
+    t.npoints = len(points)
+    for i, (sv, c) in enumerate(zip(points, rgba)):
+        t.s[i] = sv
+        for k in range(4):
+            t.rgba[i][k] = c[k]
+    t.vmin, t.vmax, t.base_step = float(vmin), float(vmax), float(base_step)
+    return t
+
+
 class inr_view(ctypes.Structure):
     _fields_ = [("base", ctypes.c_void_p), ("lo", ctypes.c_int64 * 3), ("dims", ctypes.c_int32 * 3),
                 ("stride", ctypes.c_int64 * 3), ("channels", ctypes.c_int32)]
@@ -108,6 +134,13 @@ _SIG = {
                                ctypes.POINTER(_I64), ctypes.c_double, _P, _I32, ctypes.c_double, _I32, _P, _P, _P,
                                _P]),
     "inr_pathlines": (_I32, [_P, _I32, _P, _I32, ctypes.c_double, _I32, _P, _P, _P, _P]),
+    "inr_renderer_create": (_I32, [_PP, _I32, _I32, ctypes.c_double, _P, _PP]),
+    "inr_renderer_destroy": (_I32, [_P]),
+    "inr_render": (_I32, [_P, ctypes.POINTER(inr_camera), ctypes.POINTER(inr_transfer_fn),
+                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.c_double,
+                          ctypes.c_double, _I32, _P, _P]),
+    "inr_render_stats": (_I32, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+    "inr_composite": (_I32, [_P, _I32, _I64, ctypes.POINTER(ctypes.c_float), _P, _P]),
     "inr_get_params": (_I32, [_P, _P, _I64]),
     "inr_set_params": (_I32, [_P, _P, _I64]),
     "inr_get_grads": (_I32, [_P, _P, _I64]),
@@ -252,6 +285,34 @@ def inr_trace_grids(grid_ptrs, times, dims, sign, seeds_ptr, nseeds, dt, max_ste
 def inr_pathlines(cache, window_ops, seeds_ptr, nseeds, dt, max_steps, vert_ptr, counts_ptr, reasons_ptr, stream=0):
     _check(_lib.inr_pathlines(cache, window_ops, seeds_ptr, nseeds, float(dt), max_steps, vert_ptr, counts_ptr,
                               reasons_ptr, stream))
+
+
+# ---- volume rendering (NEXT-3)
+def inr_renderer_create(models, cells=16, pad=0.0, stream=0):
+    pp, keep = _ptrs(models)
+    h = ctypes.c_void_p()
+    _check(_lib.inr_renderer_create(pp, len(models), cells, float(pad), stream, ctypes.byref(h)))
+    return h
+
+
+def inr_renderer_destroy(r):
+    _check(_lib.inr_renderer_destroy(r))
+
+
+def inr_render(r, cam, tf, lo, hi, step, frag_ptr, stop_alpha=0.99, use_macrocells=1, stream=0):
+    _check(_lib.inr_render(r, ctypes.byref(cam), ctypes.byref(tf), (ctypes.c_double * 3)(*lo),
+                           (ctypes.c_double * 3)(*hi), float(step), float(stop_alpha), int(use_macrocells), frag_ptr,
+                           stream))
+
+
+def inr_render_stats(r):
+    e, s, w = _I64(), _I64(), _I32()
+    _check(_lib.inr_render_stats(r, ctypes.byref(e), ctypes.byref(s), ctypes.byref(w)))
+    return e.value, s.value, w.value
+
+
+def inr_composite(frag_ptr, nfrag, npixels, bg, img_ptr, stream=0):
+    _check(_lib.inr_composite(frag_ptr, nfrag, npixels, (ctypes.c_float * 3)(*bg), img_ptr, stream))
 
 
 # ---- cache

@@ -83,3 +83,11 @@ def test_center_ray_points_at_the_look_point():
     th = math.tan(math.radians(20.0))
     a, b = (2 * 0.5 / 3 - 1) * th, (1 - 2 * 0.5 / 3) * th
     assert abs(math.atan2(math.hypot(d[0][0], d[0][1]), d[0][2]) - math.atan(math.hypot(a, b))) < 1e-12
+
+
+def test_batched_field_equals_per_sample_field():
+    field = lambda p: 0.5 + 0.5 * math.sin(0.3 * p[0] - 0.2 * p[2])
+    f = tf([0.0, 0.5, 1.0], [[0, 0, 1, 0.0], [0, 1, 0, 0.3], [1, 0, 0, 0.9]])
+    a = R.render_brick(field, CAM, LO, HI, 0.5, f)
+    b = R.render_brick(None, CAM, LO, HI, 0.5, f, batch_field=lambda P: np.array([field(p) for p in P]))
+    assert np.array_equal(a, b)
