@@ -390,6 +390,57 @@ def run_next2(stream, prec, n=256, window=10, steps=500, M=1 << 16, dt=0.1, amp=
     return r
 
 
+def run_next3(stream, prec, n=256, steps=1000, width=1024, height=1024):
+    """NEXT-3: direct-query volume rendering of the cfg2 DNR
+    (G2 256^3, 8 blocks, fitted 1000 steps) at 1024^2, sample streaming over the
+    tensor-core query decode, with and without macro-cell skipping; the
+    single-rank sort-last path (DNR.render) for the full frame time."""
+    dev = torch.device("cuda")
+    d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
+    vol = gen_local("g2", (n, n, n), d.lo, d.hi, dev)
+    vmin, vmax = d.value_range(vol, stream)
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = 16384
+    d.fit(vol, steps, 65536, opts, stream, report=True)
+    del vol
+    cam = inr.make_camera((-180.0, 330.0, -260.0), (128.0, 110.0, 128.0), (0.0, 1.0, 0.0), 34.0, width, height)
+    tf = inr.make_tf([0.0, 0.3, 0.45, 0.7, 1.0],
+                     [[0.0, 0.0, 0.0, 0.0], [0.0, 0.0, 0.0, 0.0], [0.1, 0.4, 1.0, 0.02], [1.0, 0.8, 0.1, 0.15],
+                      [1.0, 0.1, 0.0, 0.6]], vmin, vmax, 1.0)
+    step = 0.5
+    r = inr.inr_renderer_create(d.models, 16, 1e-3 * (vmax - vmin), stream)
+    frag = torch.empty((width * height, 5), device=dev)
+    out = {}
+    for mc in (0, 1):
+        inr.inr_render(r, cam, tf, d.lo, d.hi, step, frag.data_ptr(), 0.99, mc, stream)   # warm
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        inr.inr_render(r, cam, tf, d.lo, d.hi, step, frag.data_ptr(), 0.99, mc, stream)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        evald, skipped, waves = inr.inr_render_stats(r)
+        out["macrocells" if mc else "no_macrocells"] = {
+            "ms": ms, "samples_evaluated": evald, "samples_skipped": skipped, "waves": waves,
+            "evaluated_samples_per_s": evald / (ms / 1e3), "rays_per_s": width * height / (ms / 1e3)}
+    alpha = frag[:, 3].float()
+    coverage = float((alpha > 0.01).float().mean())
+    inr.inr_renderer_destroy(r)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    img = d.render(cam, tf, step, stream=stream)
+    e1.record()
+    torch.cuda.synchronize()
+    res = {"config": "NEXT-3 direct-query DVR of the cfg2 DNR (G2 256^3, 8 blocks), 1024^2, step 0.5",
+           "precision": "fp16" if prec else "fp32", "fit_steps": steps, "image": [width, height],
+           "coverage_alpha_gt_0.01": coverage, "mean_alpha": float(img[:, 3].mean()),
+           "frame_ms_dnr_render": e0.elapsed_time(e1), **out}
+    d.close()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="cfg1,cfg2,cfg2r,cfg3,cfg4,cfg5")
@@ -399,12 +450,12 @@ def main():
     torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
     fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg2r": run_cfg2r, "cfg3": run_cfg3, "cfg4": run_cfg4,
-           "cfg5": run_cfg5, "next2": run_next2}
+           "cfg5": run_cfg5, "next2": run_next2, "next3": run_next3}
     results = []
     for name in a.only.split(","):
         for p in a.precision.split(","):
             prec = inr.INR_PREC_FP16_MLP if p == "fp16" else inr.INR_PREC_FP32
-            if name in ("cfg2r", "cfg3", "cfg4", "cfg5", "next2") and p == "fp32":
+            if name in ("cfg2r", "cfg3", "cfg4", "cfg5", "next2", "next3") and p == "fp32":
                 continue          # the fp32 CUDA-core path is the parity mode; large configs run fp16
             t0 = time.time()
             r = fns[name](stream, prec)

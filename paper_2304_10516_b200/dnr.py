@@ -103,6 +103,18 @@ def allgather_metadata(rows):
     return [r for part in out for r in part]
 
 
+def gather_fragments(frag, dst=0):
+    """Sort-last exchange: every rank's fragment image [npix][5]
+    (C_r, C_g, C_b, A, t_enter) to rank `dst`, stacked [world][npix][5] there
+    (None elsewhere).  The depth sort happens in inr_composite."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return frag[None]
+    rank = dist.get_rank()
+    parts = [torch.empty_like(frag) for _ in range(dist.get_world_size())] if rank == dst else None
+    dist.gather(frag.contiguous(), parts, dst=dst)
+    return torch.stack(parts) if rank == dst else None
+
+
 def gather_slabs(local_core, lo, global_dims, dst=0):
     """Gather every rank's decoded core slab [z][y][x] (origin `lo`, (x, y, z))
     into the global volume on rank `dst`.
@@ -229,6 +241,31 @@ class DNR:
             refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
             self.inr.inr_decode_grid(m, res, base.data_ptr(), self._strides(nx, ny), refp,
                                      sse.data_ptr() if sse is not None else None, stream, count=cnt)
+
+    def render(self, cam, tf, step, background=(0.0, 0.0, 0.0), stop_alpha=0.99, cells=16, use_macrocells=True,
+               stream=0, dst=0):
+        """Sort-last DNR volume rendering (NEXT-3): this rank ray-marches
+        its brick [lo, hi] (its blocks' span; neighbouring bricks share a face plane,
+        the half-open sample intervals split it) by direct queries, the fragments
+        are gathered to `dst` and depth-composited there.  cam / tf: inr_camera /
+        inr_transfer_fn.  Returns the RGBA image [H*W][4] on `dst`, None elsewhere."""
+        span = float(tf.vmax - tf.vmin)
+        r = self.inr.inr_renderer_create(self.models, cells, 1e-3 * span, stream)
+        try:
+            npix = cam.width * cam.height
+            frag = torch.empty((npix, 5), dtype=torch.float32, device=torch.device("cuda", self.device))
+            self.inr.inr_render(r, cam, tf, [float(v) for v in self.lo], [float(v) for v in self.hi], step,
+                                frag.data_ptr(), stop_alpha, int(use_macrocells), stream)
+            self.last_render_stats = self.inr.inr_render_stats(r)
+        finally:
+            self.inr.inr_renderer_destroy(r)
+        torch.cuda.current_stream().synchronize()
+        frags = gather_fragments(frag, dst)
+        if frags is None:
+            return None
+        img = torch.empty((npix, 4), dtype=torch.float32, device=frag.device)
+        self.inr.inr_composite(frags.data_ptr(), frags.shape[0], npix, background, img.data_ptr(), stream)
+        return img
 
     def core_box(self):
         """(lo, hi inclusive) of this rank's core nodes (the ghost layer excluded)."""

@@ -58,7 +58,12 @@ def _worker(rank, world, port, q):
     ok = None
     if rank == 0:
         ok = bool((vol[0:2] == 1).all() and (vol[2:5] == 2).all())
-    q.put((rank, rng, sse, meta, mx, ok))
+    # sort-last fragments (NEXT-3): every rank's [npix][5] image stacked in rank order on rank 0
+    frag = torch.full((6, 5), float(rank)) + torch.arange(6.0)[:, None]
+    fr = dnr.gather_fragments(frag)
+    fok = None if fr is None else bool(fr.shape == (2, 6, 5) and (fr[1] - fr[0] == 1).all())
+    vrng = dnr.allreduce_range([lo, 2.0 * lo], [hi, 3.0 * hi])     # per-channel ranges (vector fields)
+    q.put((rank, rng, sse, meta, mx, (ok, fok), vrng))
     dist.destroy_process_group()
 
 
@@ -72,8 +77,9 @@ def test_collectives_world2_gloo():
     res = sorted(q.get(timeout=120) for _ in range(2))
     for p in ps:
         p.join(60)
-    assert res[0][5] is True and res[1][5] is None     # slab gather to rank 0 (a18)
-    for rank, rng, sse, meta, mx, _ in res:
+    assert res[0][5] == (True, True) and res[1][5] == (None, None)     # slab / fragment gathers to rank 0
+    for rank, rng, sse, meta, mx, _, vrng in res:
+        assert vrng == ([-2.0, -4.0], [1.0, 3.0])
         assert rng == (-2.0, 1.0)                         # S:L275-277 example
         assert sse == [1.5, 200.0]
         assert meta == [[0.0, 10.0], [1.0, 11.0]]
