@@ -184,6 +184,14 @@ INR_API inr_status inr_fit_group(inr_model* const* models, const inr_view* views
                          int32_t steps, int32_t batch, const inr_fit_opts* opts,
                          inr_fit_report* out, cudaStream_t stream);
 
+/* Stream-ordered report of the models' last fit step, for pipelined loops that
+ * must not synchronize per step: enqueues one kernel writing, per model i,
+ * out[3i..3i+2] = (L1_uniform, L1_boundary, 1.0 if a non-finite loss or
+ * parameter appeared else 0.0) as inr_fit_report would.  out: device memory or
+ * pinned host memory (mapped under unified addressing); read it after the
+ * stream reaches this point (e.g. an event).  Asynchronous. */
+INR_API inr_status inr_fit_losses(inr_model* const* models, int32_t nmodels, double* out, cudaStream_t stream);
+
 /* Direct queries: xyz (dev) holds q global node
  * coordinates (x,y,z interleaved); out (dev) receives q x D values in data units
  * v = Phi(x) (vmax - vmin) + vmin (per channel, channels interleaved).  A query p goes to the block

@@ -178,6 +178,7 @@ struct inr_model {
   int nfaces = 0;
   int faces[6] = {0, 0, 0, 0, 0, 0};
   float vmin[kMaxD] = {0.f, 0.f, 0.f}, vmax[kMaxD] = {1.f, 1.f, 1.f};   // per-channel range of the last fit
+  double last_inv_u = 0.0, last_inv_b = 0.0;   // 1/(B_u D), 1/(B_b D) of the last fit step (report)
   bool frozen = false;       // cache snapshot: parameters only
   bool host_resident = false;
   float* host_params = nullptr;  // pinned copy (host-resident snapshot)
@@ -546,11 +547,15 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   as.ob2 = (float)(1.0 - opts->beta2);
   as.eps = (float)opts->eps;
 
-  for (int i = 0; i < nmodels; ++i)
+  for (int i = 0; i < nmodels; ++i) {
     for (int c = 0; c < D; ++c) {
       models[i]->vmin[c] = (float)lo[c];
       models[i]->vmax[c] = (float)hi[c];
     }
+    const int bb = models[i]->nfaces > 0 ? opts->boundary_batch : 0;
+    models[i]->last_inv_u = 1.0 / ((double)batch * D);
+    models[i]->last_inv_b = bb > 0 ? 1.0 / ((double)bb * D) : 0.0;
+  }
   const int nchunks = (nmodels + kMaxGroup - 1) / kMaxGroup;
   std::vector<GroupArgs> groups(nchunks);
   for (int c = 0; c < nchunks; ++c) {
@@ -682,6 +687,27 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   }
   if (nonfinite) return fail(INR_ERR_NONFINITE, "non-finite loss or parameter after %d steps", taken);
   if (all_constant) g_err = "warning: constant field (vmax == vmin), targets are 0";
+  return INR_OK;
+}
+
+extern "C" inr_status inr_fit_losses(inr_model* const* models, int32_t nmodels, double* out, cudaStream_t st) {
+  if (!models || !out || nmodels < 1) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  for (int c0 = 0; c0 < nmodels; c0 += kMaxGroup) {
+    LossReportArgs a;
+    memset(&a, 0, sizeof a);
+    a.n = std::min(kMaxGroup, nmodels - c0);
+    for (int j = 0; j < a.n; ++j) {
+      const inr_model* m = models[c0 + j];
+      if (!m || m->frozen) return fail(INR_ERR_INVALID_ARG, "model %d is NULL or frozen", c0 + j);
+      a.acc[j] = m->acc;
+      a.flag[j] = m->flag;
+      a.inv_u[j] = m->last_inv_u;
+      a.inv_b[j] = m->last_inv_b;
+    }
+    CK(cudaSetDevice(models[c0]->device));
+    launch_loss_report(a, out + 3 * (size_t)c0, st);
+  }
+  CK_LAUNCH("loss report");
   return INR_OK;
 }
 

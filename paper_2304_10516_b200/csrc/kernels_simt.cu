@@ -382,6 +382,23 @@ __global__ void __launch_bounds__(kTile) probe_simt_kernel(GroupArgs g) {
   if ((t & 31) == 0) atomicAdd(md.acc + 2, e);
 }
 
+// ------------------------------------------------------ stream-ordered report
+// out[3 i .. 3 i + 2] = (L1_uniform, L1_boundary, non-finite flag) of model i's last step
+__global__ void loss_report_kernel(LossReportArgs a, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const double u = a.acc[i][0], b = a.acc[i][1];
+  const int bad = *a.flag[i];
+  out[3 * i] = u * a.inv_u[i];
+  out[3 * i + 1] = b * a.inv_b[i];
+  out[3 * i + 2] = (bad || !isfinite(u) || !isfinite(b)) ? 1.0 : 0.0;
+}
+
+void launch_loss_report(const LossReportArgs& a, double* out, cudaStream_t st) {
+  loss_report_kernel<<<1, 64, 0, st>>>(a, out);
+  count_launch();
+}
+
 // ------------------------------------------------------- fp16 cache storage
 __global__ void convert_f32_f16_kernel(const float* __restrict__ s, __half* __restrict__ d, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

@@ -40,6 +40,15 @@ inline int qa_nmodels(const QueryArgs& qa) { return qa.nmodels; }
 
 void count_launch(long long n = 1);
 
+// stream-ordered loss report (kernels_simt.cu)
+struct LossReportArgs {
+  int n;
+  const double* acc[kMaxGroup];
+  const int* flag[kMaxGroup];
+  double inv_u[kMaxGroup], inv_b[kMaxGroup];
+};
+void launch_loss_report(const LossReportArgs& a, double* out, cudaStream_t st);
+
 // volume rendering (kernels_render.cu, NEXT-3)
 constexpr int kTfMaxPoints = 16;
 constexpr int kMaxFragments = 64;

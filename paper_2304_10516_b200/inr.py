@@ -117,6 +117,7 @@ _SIG = {
                        ctypes.POINTER(inr_fit_report), _P]),
     "inr_fit_group": (_I32, [_PP, ctypes.POINTER(inr_view), _I32, _I32, _I32, ctypes.POINTER(inr_fit_opts),
                              ctypes.POINTER(inr_fit_report), _P]),
+    "inr_fit_losses": (_I32, [_PP, _I32, _P, _P]),
     "inr_decode": (_I32, [_P, _P, _I64, _P, _I32, _P]),
     "inr_decode_group": (_I32, [_PP, _I32, _P, _I64, _P, _I32, _P]),
     "inr_decode_grid": (_I32, [_P, ctypes.POINTER(_I32), _P, ctypes.POINTER(_I64), _P, _P, _P]),
@@ -245,6 +246,12 @@ def inr_fit_group(models, views, steps, batch, opts, stream=0, report=True):
     reps = (inr_fit_report * len(models))() if report else None
     _check(_lib.inr_fit_group(pp, va, len(models), steps, batch, ctypes.byref(opts), reps, stream))
     return list(reps) if reps is not None else None
+
+
+def inr_fit_losses(models, out_ptr, stream=0):
+    """Enqueue the (L1_u, L1_b, nonfinite) report of every model's last step into out (3 doubles per model)."""
+    pp, keep = _ptrs(models)
+    _check(_lib.inr_fit_losses(pp, len(models), out_ptr, stream))
 
 
 def inr_decode(m, xyz_ptr, q, out_ptr, strict=0, stream=0):

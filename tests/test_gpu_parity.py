@@ -566,3 +566,25 @@ def test_view_is_read_only_inside_its_contract(prec):
     assert np.array_equal(get_params(a), get_params(b))
     inr.inr_destroy(a)
     inr.inr_destroy(b)
+
+
+def test_stream_ordered_loss_report_matches_fit_report():
+    """inr_fit_losses (no synchronization) reports the same L1 terms as the
+    synchronous inr_fit_report of the same step, per model of a group."""
+    vol = synth.g1_analytic(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
+    ms = [make_gpu_model(b, 3, precision=1, **CFG1) for b in blocks]
+    reps = inr.inr_fit_group(ms, [whole_view(vt)] * len(ms), 3, 256, go, stream(), True)
+    out = torch.full((3 * len(ms),), float("nan"), dtype=torch.float64, device="cuda")
+    inr.inr_fit_losses(ms, out.data_ptr(), stream())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(-1, 3)
+    for r, row in zip(reps, o):
+        assert abs(row[0] - r.loss_uniform) <= 1e-15 * r.loss_uniform
+        assert abs(row[1] - r.loss_boundary) <= 1e-15 * max(r.loss_boundary, 1e-300)
+        assert row[2] == 0.0
+    for m in ms:
+        inr.inr_destroy(m)
