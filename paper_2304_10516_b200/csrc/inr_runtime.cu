@@ -818,7 +818,7 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
     g->net = qa->net;
     g->nmodels = nmodels;
     for (int i = 0; i < nmodels; ++i) g->md[i] = qa->md[i];
-    { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_tc(*g, xyz, q, out, qb.perm, qb.tile_slot, qb.ntiles, st); }
+    { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_tc(*g, xyz, q, out, qb, st); }
     delete g;
     cudaFreeAsync(ws, st);
   } else if (q > 0) {

@@ -172,6 +172,58 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
   scatter_chunk<F>(g, md, m, l, samples, dfeat, Bs, i0, min(i0 + kBwdChunk, total), acc_raw);
 }
 
+// ---------------------------------------------- level-major query encode
+// Bucketed queries [c0*128, c0*128 + n) -> qx[j] = (x, y, z, slot bits): the
+// block-normalized coordinate x = fl32(fl32(p - o) / n) (R5); slot -1 = padding.
+__global__ void query_prep_kernel(GroupArgs g, const float* __restrict__ xyz, const int* __restrict__ perm,
+                                  const int* __restrict__ tile_slot, const int* __restrict__ ntiles, long long j0,
+                                  long long n, float4* __restrict__ qx) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const long long jj = j0 + j;
+  const int qi = jj < (long long)*ntiles * 128 ? perm[jj] : -1;
+  if (qi < 0) { qx[j] = make_float4(0.f, 0.f, 0.f, __int_as_float(-1)); return; }
+  const int slot = tile_slot[jj >> 7];
+  const ModelDev& md = g.md[slot];
+  float x[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    x[d] = __fdiv_rn(__fsub_rn(__ldg(xyz + 3 * (long long)qi + d), (float)md.o[d]), (float)md.n[d]);
+  qx[j] = make_float4(x[0], x[1], x[2], __int_as_float(slot));
+}
+
+// Level-major (grid.y = level): the CTAs in flight gather from one level of every
+// block (<= 8 x 4 MB at cfg2) instead of all levels of one or two blocks, so the
+// tables stay L2-resident as in the fit's encode_fwd_kernel.  Writes the fp16 h_0
+// tile images of the tensor-core forward (forward layout: no ones group).
+template <int F>
+__global__ void __launch_bounds__(kLmThreads) encode_query_kernel(GroupArgs g, const float4* __restrict__ qx,
+                                                                   long long n, uint8_t* __restrict__ featimg,
+                                                                   FeatGeom geom) {
+  const int l = blockIdx.y;
+  const long long j = blockIdx.x * (long long)kLmThreads + threadIdx.x;
+  if (j >= n) return;
+  const float4 s = __ldg(qx + j);
+  const int slot = __float_as_int(s.w);
+  float f[F];
+#pragma unroll
+  for (int k = 0; k < F; ++k) f[k] = 0.f;
+  if (slot >= 0) {
+    const float x[3] = {s.x, s.y, s.z};
+    encode_level<F>(g.md[slot].params, g.net.lv[l], g.net.table_mask, x, f);
+  }
+  const int r = (int)(j & 127);
+  uint8_t* row = featimg + (size_t)(j >> 7) * geom.tile_bytes + (r & 7) * 16 + (r >> 3) * geom.sbo;
+  const int c = l * F;
+  if constexpr (F == 1) {
+    *reinterpret_cast<__half*>(row + (c >> 3) * 128 + (c & 7) * 2) = __float2half_rn(f[0]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < F; k += 2)
+      *reinterpret_cast<__half2*>(row + ((c + k) >> 3) * 128 + ((c + k) & 7) * 2) = __floats2half2_rn(f[k], f[k + 1]);
+  }
+}
+
 // ------------------------------------------------------- query bucketing
 // Decode queries on tensor cores need every 128-query tile to come from one
 // block: route each query to its block (R5), count per block, lay the blocks'
@@ -255,6 +307,12 @@ void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, fl
   count_launch(3);
 }
 
+void launch_query_prep(const GroupArgs& g, const float* xyz, const QueryBuckets& b, long long j0, long long n,
+                       float4* qx, cudaStream_t st) {
+  query_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g, xyz, b.perm, b.tile_slot, b.ntiles, j0, n, qx);
+  count_launch();
+}
+
 // ============================================================ host launchers
 #define LM_DISPATCH_F(F_, ...)                           \
   switch (F_) {                                          \
@@ -291,6 +349,13 @@ LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs) {
   w.targets = net.D > 1 ? reinterpret_cast<float4*>(p) : nullptr;
   w.Bs = Bs;
   return w;
+}
+
+void launch_encode_query(const GroupArgs& g, const float4* qx, long long n, uint8_t* featimg, const FeatGeom& geom,
+                         cudaStream_t st) {
+  dim3 grid((unsigned)((n + kLmThreads - 1) / kLmThreads), g.net.L);
+  LM_DISPATCH_F(g.net.F, encode_query_kernel<FF><<<grid, kLmThreads, 0, st>>>(g, qx, n, featimg, geom));
+  count_launch();
 }
 
 void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st) {

@@ -520,8 +520,9 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
 //   MODE 0  debug: block-normalized x01[q] -> y[q] (normalized units)
 //   MODE 1  decode grid: x_j = fl32(j / R) lattice of one block, denormalized
 //           strided stores, optional fused SSE against ref (R18, R19)
-//   MODE 2  decode query: tiles of bucket-sorted query indices, every tile from
-//           one block (see the bucketing kernels below), x = fl32(fl32(p-o)/n)
+//   MODE 3  decode query: tiles of bucket-sorted queries, every tile from one
+//           block, whose fp16 h_0 tile images were encoded level-major
+//           (encode_query_kernel, kernels_lm.cu) and arrive by TMA bulk copy
 struct FwdArgs {
   const float* x01;
   float* y;
@@ -536,6 +537,8 @@ struct FwdArgs {
   const int* tile_slot;
   const int* ntiles_dev;
   const uint8_t* wimg;   // prepared weight images, one per model slot (prep_image_kernel)
+  const uint8_t* featimg;   // MODE 3: h_0 tile images of tiles [tile0, tile1)
+  long long tile0, tile1;
 };
 
 template <int F, int MODE, int D>
@@ -548,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
   const uint32_t mbar = smem_u32(smem + lay.mbar);
   const uint32_t mbar_img = smem_u32(smem + lay.mbar_img);
+  const uint32_t mbar_feat = smem_u32(smem + lay.mbar_feat[0]);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + lay.tslot);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
@@ -557,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   if (t == 0) {
     mbar_init(mbar, 1);
     mbar_init(mbar_img, 1);
+    mbar_init(mbar_feat, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_before();
@@ -564,18 +569,18 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  uint32_t phase = 0, img_phase = 0;
+  uint32_t phase = 0, img_phase = 0, feat_phase = 0;
   int cur = -1;  // model whose weight image is in smem
   // tiles are visited grid-stride: the CTAs in flight work on consecutive tiles,
   // i.e. (MODE 2, tiles grouped by block) on one or two blocks' tables at a time;
   // a CTA reloads weights only when its next tile belongs to another block
-  long long ntiles;
-  if constexpr (MODE == 0) ntiles = (a.q + kTileM - 1) / kTileM;
-  else if constexpr (MODE == 1) ntiles = ((long long)a.cnt[0] * a.cnt[1] * a.cnt[2] + kTileM - 1) / kTileM;
-  else ntiles = *a.ntiles_dev;
-  const long long t0 = blockIdx.x, t1 = ntiles, tstep = gridDim.x;
+  long long t0 = blockIdx.x, t1;
+  if constexpr (MODE == 0) t1 = (a.q + kTileM - 1) / kTileM;
+  else if constexpr (MODE == 1) t1 = ((long long)a.cnt[0] * a.cnt[1] * a.cnt[2] + kTileM - 1) / kTileM;
+  else { t0 += a.tile0; t1 = min(a.tile1, (long long)*a.ntiles_dev); }
+  const long long tstep = gridDim.x;
   for (long long tile = t0; tile < t1; tile += tstep) {
-    const int slot = MODE == 2 ? a.tile_slot[tile] : 0;
+    const int slot = MODE == 3 ? a.tile_slot[tile] : 0;
     if (slot != cur) {   // one TMA bulk copy of this block's prepared weight image
       __syncthreads();
       if (t == 0) {
@@ -609,14 +614,17 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
     } else {
       const int qi = a.perm[j];
       valid = qi >= 0;
-      if (valid) {
-        dst = qi;
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-          x[d] = __fdiv_rn(__fsub_rn(__ldg(a.xyz + 3 * (long long)qi + d), (float)md.o[d]), (float)md.n[d]);
-      }
+      dst = qi;
     }
-    {
+    if constexpr (MODE == 3) {   // the level-major encoded h_0 tile, one bulk copy
+      if (t == 0) {
+        mbar_expect_tx(mbar_feat, lay.feat_tile_bytes);
+        bulk_g2s(smem_u32(smem + lay.h[0]), a.featimg + (size_t)(tile - a.tile0) * lay.feat_tile_bytes,
+                 lay.feat_tile_bytes, mbar_feat);
+      }
+      mbar_wait(mbar_feat, feat_phase);
+      feat_phase ^= 1;
+    } else {
       // features straight into this thread's row of the h_0 tile (no staging array)
       uint8_t* row = smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0];
 #pragma unroll 4
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
     } else {
       double e = 0.0;
       if (valid) {
-        if constexpr (MODE == 2) dst *= D;   // query outputs: q x D, channels interleaved
+        if constexpr (MODE == 3) dst *= D;   // query outputs: q x D, channels interleaved
 #pragma unroll
         for (int c = 0; c < D; ++c) {
           const float v = fmaf(y[c], md.vrange[c], md.vmin[c]);
@@ -766,16 +774,40 @@ void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res
   launch_forward<1>(*single_group(net, md), a, (n + kTileM - 1) / kTileM, st);
 }
 
-void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const int* perm,
-                            const int* tile_slot, const int* ntiles_dev, cudaStream_t st) {
-  FwdArgs a;
-  memset(&a, 0, sizeof a);
-  a.xyz = xyz;
-  a.out = out;
-  a.perm = perm;
-  a.tile_slot = tile_slot;
-  a.ntiles_dev = ntiles_dev;
-  launch_forward<2>(g, a, (q + kTileM - 1) / kTileM + g.nmodels, st);
+// Queries: per chunk of <= 2^15 bucketed tiles, x per query (query_prep_kernel),
+// level-major fp16 encode into tile images (encode_query_kernel), then the
+// tensor-core MLP over the tiles (MODE 3).  Stream-ordered chunk workspace.
+void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const QueryBuckets& b,
+                            cudaStream_t st) {
+  Layout L;
+  if (!build_layout(g.net, L, false)) return;
+  const long long ub = q / kTileM + g.nmodels + 1;        // upper bound of the device tile count
+  const long long chunk = std::min<long long>(ub, 1ll << 15);
+  FeatGeom geom;
+  geom.sbo = L.h_sbo[0];
+  geom.tile_bytes = L.feat_tile_bytes;
+  geom.ones = 0;
+  uint8_t* ws = nullptr;
+  const size_t qx_bytes = (size_t)chunk * kTileM * sizeof(float4);
+  if (cudaMallocAsync((void**)&ws, qx_bytes + (size_t)chunk * L.feat_tile_bytes, st) != cudaSuccess) return;
+  float4* qx = reinterpret_cast<float4*>(ws);
+  uint8_t* featimg = ws + qx_bytes;
+  for (long long c0 = 0; c0 < ub; c0 += chunk) {
+    const long long nt = std::min(chunk, ub - c0);
+    launch_query_prep(g, xyz, b, c0 * kTileM, nt * kTileM, qx, st);
+    launch_encode_query(g, qx, nt * kTileM, featimg, geom, st);
+    FwdArgs a;
+    memset(&a, 0, sizeof a);
+    a.out = out;
+    a.perm = b.perm;
+    a.tile_slot = b.tile_slot;
+    a.ntiles_dev = b.ntiles;
+    a.featimg = featimg;
+    a.tile0 = c0;
+    a.tile1 = c0 + nt;
+    launch_forward<3>(g, a, nt, st);
+  }
+  cudaFreeAsync(ws, st);
 }
 
 }  // namespace inr

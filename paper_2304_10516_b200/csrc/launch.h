@@ -148,14 +148,18 @@ void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x0
                              cudaStream_t st);
 void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                            const long long os[3], const float* ref, double* sse, cudaStream_t st);
-void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const int* perm,
-                            const int* tile_slot, const int* ntiles_dev, cudaStream_t st);
 struct QueryBuckets {
   int* perm;       // [q + 128 nmodels] query index or -1, bucket-sorted, each bucket padded to 128
   int* tile_slot;  // model slot of each 128-query tile
   int* ntiles;     // device scalar
 };
+void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, float* out, const QueryBuckets& b,
+                            cudaStream_t st);
 size_t query_workspace_bytes(long long q, int nmodels);
+void launch_query_prep(const GroupArgs& g, const float* xyz, const QueryBuckets& b, long long j0, long long n,
+                       float4* qx, cudaStream_t st);
+void launch_encode_query(const GroupArgs& g, const float4* qx, long long n, uint8_t* featimg, const FeatGeom& geom,
+                         cudaStream_t st);
 void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, float* out, int* dflag, void* ws,
                           QueryBuckets& b, cudaStream_t st);
 
