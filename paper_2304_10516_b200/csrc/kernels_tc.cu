@@ -782,7 +782,8 @@ void launch_decode_query_tc(const GroupArgs& g, const float* xyz, long long q, f
   Layout L;
   if (!build_layout(g.net, L, false)) return;
   const long long ub = q / kTileM + g.nmodels + 1;        // upper bound of the device tile count
-  const long long chunk = std::min<long long>(ub, 1ll << 15);
+  const long long nchunks = (ub + (1ll << 15) - 1) >> 15;   // balanced chunks of <= ~2^15 tiles
+  const long long chunk = (ub + nchunks - 1) / nchunks;
   FeatGeom geom;
   geom.sbo = L.h_sbo[0];
   geom.tile_bytes = L.feat_tile_bytes;
