@@ -159,6 +159,25 @@ class Clocks:
                 "samples_total": n_all}
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` from the
+    committed ncu --set full capture (profiles/), in bytes, or None."""
+    name = {"adam": "adam_kernel", "mlp_tc": "mlp_fit_kernel", "encode_bwd": "encode_bwd_kernel",
+            "encode_fwd": "encode_fwd_kernel"}.get(kernel, kernel)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_final_ncu_full.txt")
+    try:
+        blk = None
+        for line in open(path):
+            if line.startswith("["):
+                blk = line.strip()
+            elif blk and name in blk and line.strip().startswith("traffic (read+write)"):
+                return float(line.split()[-2]) * 1e9, os.path.relpath(path, os.path.dirname(path) + "/..") + \
+                    " (ncu --set full, one launch, Gbyte x 1e9)"
+    except OSError:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------- our arm
 def run_ours(args):
     import numpy as np
@@ -253,6 +272,9 @@ def run_ours(args):
                 "unit": "TFLOP/s", "traffic": None, "algorithmic_flop_per_launch": flop,
                 "l2_gather_scatter_bytes_per_launch": 2 * 8 * 16 * 2 * 4.0 * coords_per_step}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    tr = ncu_traffic(roof["kernel"])
+    if tr is not None:
+        roof["traffic"], roof["traffic_source"] = tr
     roof["peak_source"] = pv
     roof["avg_launch_ms"] = avg_s * 1e3
     roof["share_of_step"] = dom_ms / ms
