@@ -1,0 +1,118 @@
+"""Degenerate and boundary cases through the C ABI (SURVEY §8(c) "edge cases"):
+empty inputs, single-point lattices, a 1-node-thick upper block, the domain
+corners, NaN routing of absent blocks, zero-seed traces, 1x1 renders."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import decode as o_decode, sampler
+from oracle.model import InrModel
+from paper_2304_10516_b200 import inr
+
+from gpu_util import gpu_volume, make_gpu_model, normwise, oracle_config, stream, whole_view
+
+pytestmark = pytest.mark.gpu
+
+NET = dict(levels=8, features=2, log2_table_size=12, mlp_hidden_layers=2)
+
+
+@pytest.fixture(scope="module", params=[0, 1], ids=["fp32", "fp16"])
+def models(request):
+    vol = synth.g1_analytic(33).numpy()                    # 33^3 with 16^3 blocks: the upper layer is 1 node
+    blocks = sampler.decompose((33, 33, 33), (16, 16, 16))
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 32
+    cfg = oracle_config(**NET)
+    gms, oms = [], {}
+    for b in blocks:
+        m = make_gpu_model(b, 2, precision=request.param, **NET)
+        inr.inr_fit(m, whole_view(vt), 5, 128, go, stream())
+        p = np.empty(inr.inr_param_count(m), np.float32)
+        inr.inr_get_params(m, p)
+        om = InrModel(cfg, b, 2, params=p)
+        om.vmin, om.vmax = go.vmin, go.vmax
+        gms.append(m)
+        oms[b.block_id] = om
+    yield dict(gms=gms, oms=oms, blocks=blocks, tol=1e-5 if request.param == 0 else 2e-3)
+    for m in gms:
+        inr.inr_destroy(m)
+
+
+def test_zero_queries_is_a_no_op(models):
+    out = torch.full((4,), 7.0, device="cuda")
+    pts = torch.zeros((4, 3), device="cuda")
+    inr.inr_decode_group(models["gms"], pts.data_ptr(), 0, out.data_ptr(), 0, stream())
+    torch.cuda.synchronize()
+    assert torch.all(out == 7.0)
+
+
+def test_single_point_lattice_and_domain_corners(models):
+    gms, oms, blocks = models["gms"], models["oms"], models["blocks"]
+    out = torch.full((1,), float("nan"), device="cuda")
+    inr.inr_decode_grid(gms[0], (1, 1, 1), out.data_ptr(), None, None, None, stream())
+    corners = np.array([[0, 0, 0], [32, 32, 32], [32, 0, 0], [0, 32, 32], [16, 16, 16], [15.999, 31.5, 32]],
+                       np.float32)
+    pd = torch.from_numpy(corners).cuda()
+    q = torch.full((corners.shape[0],), float("nan"), device="cuda")
+    inr.inr_decode_group(gms, pd.data_ptr(), corners.shape[0], q.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    ref = o_decode.decode_query(oms, corners)
+    assert normwise(q.cpu().numpy(), ref) <= models["tol"]
+    g0 = o_decode.decode_grid(oms[blocks[0].block_id], (1, 1, 1))
+    assert normwise(out.cpu().numpy(), g0.reshape(-1)) <= models["tol"]
+
+
+def test_one_node_upper_block_decodes_its_node(models):
+    gms, oms, blocks = models["gms"], models["oms"], models["blocks"]
+    b = blocks[-1]
+    assert tuple(b.origin) == (32, 32, 32)
+    out = torch.full((1,), float("nan"), device="cuda")
+    inr.inr_decode_grid(gms[-1], (16, 16, 16), out.data_ptr(), (1, 1, 1), None, None, stream(), count=(1, 1, 1))
+    torch.cuda.synchronize()
+    ref = o_decode.decode_query(oms, np.array([[32, 32, 32]], np.float32))
+    assert normwise(out.cpu().numpy(), ref) <= models["tol"]
+
+
+def test_strict_queries_outside_the_domain(models):
+    pts = torch.tensor([[1.0, 2.0, 3.0], [-0.5, 0.0, 0.0]], device="cuda")
+    out = torch.empty(2, device="cuda")
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_decode_group(models["gms"], pts.data_ptr(), 2, out.data_ptr(), 1, stream())
+    assert e.value.status == inr.INR_ERR_DOMAIN
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()          # values are still written (clamped routing)
+
+
+def test_zero_seed_trace_and_all_seeds_outside():
+    g = torch.zeros((5, 5, 5, 3), device="cuda")
+    s = torch.tensor([[-1.0, 0.0, 0.0], [0.0, 9.0, 0.0]], dtype=torch.float64, device="cuda")
+    v = torch.zeros((2, 4, 5), dtype=torch.float64, device="cuda")
+    c = torch.full((2,), 9, dtype=torch.int32, device="cuda")
+    w = torch.full((2,), 9, dtype=torch.int32, device="cuda")
+    inr.inr_trace_grids([g.data_ptr(), g.data_ptr()], [0.0, 1.0], (5, 5, 5), 1.0, s.data_ptr(), 0, 0.1, 3,
+                        v.data_ptr(), c.data_ptr(), w.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert torch.all(c == 9)                  # nseeds = 0: untouched
+    inr.inr_trace_grids([g.data_ptr(), g.data_ptr()], [0.0, 1.0], (5, 5, 5), 1.0, s.data_ptr(), 2, 0.1, 3,
+                        v.data_ptr(), c.data_ptr(), w.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert torch.all(c == 0) and torch.all(w == inr.INR_PATH_OUT_OF_DOMAIN)
+
+
+def test_one_pixel_render_and_miss(models):
+    r = inr.inr_renderer_create(models["gms"], 4)
+    tf = inr.make_tf([0.0, 1.0], [[0, 0, 1, 0.1], [1, 0, 0, 0.5]], 0.0, 1.0)
+    frag = torch.full((1, 5), float("nan"), device="cuda")
+    cam = inr.make_camera((16.0, 16.0, -40.0), (16.0, 16.0, 16.0), (0.0, 1.0, 0.0), 10.0, 1, 1)
+    inr.inr_render(r, cam, tf, (0, 0, 0), (32, 32, 32), 0.5, frag.data_ptr(), stream=stream())
+    torch.cuda.synchronize()
+    f = frag.cpu().numpy()[0]
+    assert 0 < f[3] <= 1 and abs(f[4] - 40.0) < 1e-4            # enters the box at z = 0
+    away = inr.make_camera((16.0, 16.0, -40.0), (16.0, 16.0, -80.0), (0.0, 1.0, 0.0), 10.0, 1, 1)
+    inr.inr_render(r, away, tf, (0, 0, 0), (32, 32, 32), 0.5, frag.data_ptr(), stream=stream())
+    torch.cuda.synchronize()
+    f = frag.cpu().numpy()[0]
+    assert np.all(f[:4] == 0) and np.isinf(f[4])
+    inr.inr_renderer_destroy(r)
