@@ -171,8 +171,10 @@ def ncu_traffic(kernel):
             if line.startswith("["):
                 blk = line.strip()
             elif blk and name in blk and line.strip().startswith("traffic (read+write)"):
-                return float(line.split()[-2]) * 1e9, os.path.relpath(path, os.path.dirname(path) + "/..") + \
-                    " (ncu --set full, one launch, Gbyte x 1e9)"
+                val, unit = float(line.split()[-2]), line.split()[-1]
+                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+                return val * scale, os.path.relpath(path, os.path.dirname(path) + "/..") + \
+                    " (ncu --set full, one launch)"
     except OSError:
         pass
     return None

@@ -231,25 +231,32 @@ __global__ void __launch_bounds__(kLmThreads) encode_query_kernel(GroupArgs g, c
 // not deterministic, but each query's value does not depend on its tile slot.
 __global__ void route_kernel(QueryArgs qa, const float* __restrict__ xyz, long long q, int* __restrict__ slot_of,
                              int* __restrict__ counts, int* __restrict__ dflag, float* __restrict__ out) {
+  // per-CTA histogram in shared memory, one global atomic per (CTA, block): the
+  // few per-block counters would otherwise serialize every warp's atomics
+  __shared__ int cnt[kMaxGroup];
+  for (int s = threadIdx.x; s < qa.nmodels; s += blockDim.x) cnt[s] = 0;
+  __syncthreads();
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= q) return;
-  int bc[3];
-  bool outside = false;
+  if (j < q) {
+    int bc[3];
+    bool outside = false;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const float p = __ldg(xyz + 3 * j + d);
-    outside |= !(p >= 0.f && p <= (float)(qa.N[d] - 1));
-    const int b = (int)floorf(__fdiv_rn(p, (float)qa.n[d]));
-    bc[d] = min(max(b, 0), qa.B[d] - 1);
+    for (int d = 0; d < 3; ++d) {
+      const float p = __ldg(xyz + 3 * j + d);
+      outside |= !(p >= 0.f && p <= (float)(qa.N[d] - 1));
+      const int b = (int)floorf(__fdiv_rn(p, (float)qa.n[d]));
+      bc[d] = min(max(b, 0), qa.B[d] - 1);
+    }
+    const int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
+    const int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
+    slot_of[j] = slot;
+    if (slot >= 0) atomicAdd(cnt + slot, 1);
+    else out[j] = __int_as_float(0x7fc00000);
+    if (outside && dflag) atomicOr(dflag, 1);
   }
-  const int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
-  const int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
-  slot_of[j] = slot;
-  // warp-aggregated count: one atomic per distinct block in the warp
-  const unsigned peers = __match_any_sync(__activemask(), slot);
-  if (slot >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + slot, __popc(peers));
-  if (slot < 0) out[j] = __int_as_float(0x7fc00000);
-  if (outside && dflag) atomicOr(dflag, 1);
+  __syncthreads();
+  for (int s = threadIdx.x; s < qa.nmodels; s += blockDim.x)
+    if (cnt[s]) atomicAdd(counts + s, cnt[s]);
 }
 
 __global__ void bucket_offsets_kernel(const int* __restrict__ counts, int nmodels, int* __restrict__ offsets,
@@ -267,18 +274,22 @@ __global__ void bucket_offsets_kernel(const int* __restrict__ counts, int nmodel
     for (int tt = off[s] / 128 + threadIdx.x; tt < off[s + 1] / 128; tt += blockDim.x) tile_slot[tt] = s;
 }
 
-__global__ void bucket_scatter_kernel(const int* __restrict__ slot_of, long long q, const int* __restrict__ offsets,
-                                      int* __restrict__ cursor, int* __restrict__ perm) {
+__global__ void bucket_scatter_kernel(const int* __restrict__ slot_of, long long q, int nmodels,
+                                      const int* __restrict__ offsets, int* __restrict__ cursor,
+                                      int* __restrict__ perm) {
+  // rank within the CTA's share of each bucket (shared atomics), then one global
+  // reservation per (CTA, block)
+  __shared__ int cnt[kMaxGroup], base[kMaxGroup];
+  for (int s = threadIdx.x; s < nmodels; s += blockDim.x) cnt[s] = 0;
+  __syncthreads();
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= q) return;
-  const int s = slot_of[j];
-  const unsigned peers = __match_any_sync(__activemask(), s);
-  if (s < 0) return;
-  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(cursor + s, __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  perm[offsets[s] + base + __popc(peers & ((1u << lane) - 1u))] = (int)j;
+  const int s = j < q ? slot_of[j] : -1;
+  const int local = s >= 0 ? atomicAdd(cnt + s, 1) : 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < nmodels; t += blockDim.x)
+    if (cnt[t]) base[t] = atomicAdd(cursor + t, cnt[t]);
+  __syncthreads();
+  if (s >= 0) perm[offsets[s] + base[s] + local] = (int)j;
 }
 
 size_t query_workspace_bytes(long long q, int nmodels) {
@@ -303,7 +314,7 @@ void launch_query_buckets(const QueryArgs& qa, const float* xyz, long long q, fl
   const unsigned grid = (unsigned)((q + 255) / 256);
   route_kernel<<<grid, 256, 0, st>>>(qa, xyz, q, slot_of, counts, dflag, out);
   bucket_offsets_kernel<<<1, 128, 0, st>>>(counts, qa_nmodels(qa), offsets, b.tile_slot, b.ntiles);
-  bucket_scatter_kernel<<<grid, 256, 0, st>>>(slot_of, q, offsets, cursor, b.perm);
+  bucket_scatter_kernel<<<grid, 256, 0, st>>>(slot_of, q, qa_nmodels(qa), offsets, cursor, b.perm);
   count_launch(3);
 }
 
