@@ -173,10 +173,12 @@ def run_cfg3(stream, prec):
     return r
 
 
-def run_cfg4(stream, prec, timesteps=100, window=40, steps=500, cache_flags=inr.CACHE_FP16):
+def run_cfg4(stream, prec, timesteps=100, window=40, steps=500, cache_flags=inr.CACHE_FP16, warm=False):
     """Temporal cache: per timestep of an evolving G2 256^3
     field, reset + fit 500 steps, insert into a window of 40 (FIFO evicts);
-    every 10th insert decodes a random cached timestep at 256^3."""
+    every 10th insert decodes a random cached timestep at 256^3.  warm: NEXT-4
+    warm start — keep the previous timestep's network, restart Adam and the
+    learning-rate schedule (inr_reset_optimizer) instead of a fresh init."""
     n = 256
     dev = torch.device("cuda")
     d = dnr.DNR((n, n, n), (128, 128, 128), inr.make_config(precision=prec, **NET2))
@@ -191,7 +193,10 @@ def run_cfg4(stream, prec, timesteps=100, window=40, steps=500, cache_flags=inr.
         vol = gen_local("g2", (n, n, n), d.lo, d.hi, dev, tau=tau)
         d.value_range(vol, stream)
         for m in d.models:
-            inr.inr_reset(m, 0x230410516 + ti)
+            if warm and ti > 0:
+                inr.inr_reset_optimizer(m)
+            else:
+                inr.inr_reset(m, 0x230410516 + ti)
         e0, e1 = ev(), ev()
         e0.record()
         d.fit(vol, steps, 65536, opts, stream, report=True)
@@ -224,7 +229,8 @@ def run_cfg4(stream, prec, timesteps=100, window=40, steps=500, cache_flags=inr.
         # PSNR of the fresh model on its own timestep
         p, _, _ = psnr_1x(d, vol, stream)
         psnrs.append(p)
-    r = {"config": "cfg4", "precision": "fp16" if prec else "fp32", "timesteps": timesteps, "window": window,
+    r = {"config": "cfg4" + (" warm start (NEXT-4)" if warm else ""), "precision": "fp16" if prec else "fp32",
+         "timesteps": timesteps, "window": window, "init": "warm (previous timestep)" if warm else "fresh",
          "steps_per_insert": steps, "fit_ms_per_insert_mean": float(np.mean(fit_ms)),
          "fit_coords_per_s": 8 * (65536 + 16384) * steps / (np.mean(fit_ms) / 1e3),
          "psnr_db_mean": float(np.mean(psnrs)), "psnr_db_min": float(np.min(psnrs)),
@@ -450,12 +456,14 @@ def main():
     torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
     fns = {"cfg1": run_cfg1, "cfg2": run_cfg2, "cfg2r": run_cfg2r, "cfg3": run_cfg3, "cfg4": run_cfg4,
-           "cfg5": run_cfg5, "next2": run_next2, "next3": run_next3}
+           "cfg5": run_cfg5, "next2": run_next2, "next3": run_next3,
+           "cfg4w": lambda st, p: run_cfg4(st, p, steps=250, warm=True),
+           "cfg4c250": lambda st, p: run_cfg4(st, p, steps=250)}
     results = []
     for name in a.only.split(","):
         for p in a.precision.split(","):
             prec = inr.INR_PREC_FP16_MLP if p == "fp16" else inr.INR_PREC_FP32
-            if name in ("cfg2r", "cfg3", "cfg4", "cfg5", "next2", "next3") and p == "fp32":
+            if name in ("cfg2r", "cfg3", "cfg4", "cfg4w", "cfg4c250", "cfg5", "next2", "next3") and p == "fp32":
                 continue          # the fp32 CUDA-core path is the parity mode; large configs run fp16
             t0 = time.time()
             r = fns[name](stream, prec)

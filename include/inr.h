@@ -109,6 +109,11 @@ INR_API inr_status inr_create(const inr_config* cfg, const inr_block* block, int
 /* Re-initialise parameters from `seed`, zero Adam state and grads, step = 0
  * (fresh init per timestep, [R22]).  INR_ERR_STATE on a frozen model. */
 INR_API inr_status inr_reset(inr_model* m, uint64_t seed);
+/* Warm start (a semantics change versus R22's fresh init):
+ * keep the parameters, zero the Adam moments, gradients and step counter (the
+ * learning-rate schedule restarts), so the next inr_fit continues from the
+ * previous timestep's network.  INR_ERR_STATE on a frozen model. */
+INR_API inr_status inr_reset_optimizer(inr_model* m);
 /* Free a model (NULL is a no-op).  Models borrowed from a cache must not be destroyed. */
 INR_API inr_status inr_destroy(inr_model* m);
 /* Number of fp32 parameters in the declared order (tables by level, then

@@ -313,11 +313,13 @@ static inr_status alloc_model(inr_model* m, bool frozen, bool host_only = false)
   return INR_OK;
 }
 
-static inr_status init_state(inr_model* m, uint64_t seed, cudaStream_t st) {
-  uint32_t k0, k1;
-  philox_key(seed, 0, k0, k1);
-  launch_init_params(m->net, m->params, k0, k1, m->block_id, st);
-  CK_LAUNCH("init_params");
+static inr_status init_state(inr_model* m, uint64_t seed, cudaStream_t st, bool keep_params = false) {
+  if (!keep_params) {
+    uint32_t k0, k1;
+    philox_key(seed, 0, k0, k1);
+    launch_init_params(m->net, m->params, k0, k1, m->block_id, st);
+    CK_LAUNCH("init_params");
+  }
   size_t n = (size_t)m->P_pad * 4;
   CK(cudaMemsetAsync(m->grads, 0, n * 3, st));  // grads, m, v are contiguous
   if (m->gfx) CK(cudaMemsetAsync(m->gfx, 0, (size_t)m->P_pad * 8, st));
@@ -360,6 +362,17 @@ extern "C" inr_status inr_reset(inr_model* m, uint64_t seed) {
   CK(cudaDeviceSynchronize());   // work queued on any stream may still use the parameters
   m->cfg.seed = seed;
   inr_status s = init_state(m, seed, 0);
+  if (s) return s;
+  CK(cudaStreamSynchronize(0));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_reset_optimizer(inr_model* m) {
+  if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
+  if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
+  CK(cudaSetDevice(m->device));
+  CK(cudaDeviceSynchronize());
+  inr_status s = init_state(m, m->cfg.seed, 0, true);
   if (s) return s;
   CK(cudaStreamSynchronize(0));
   return INR_OK;

@@ -109,6 +109,7 @@ _SIG = {
     "inr_create": (_I32, [ctypes.POINTER(inr_config), ctypes.POINTER(inr_block), ctypes.c_int, _PP]),
     "inr_reset": (_I32, [_P, _U64]),
     "inr_destroy": (_I32, [_P]),
+    "inr_reset_optimizer": (_I32, [_P]),
     "inr_param_count": (_I32, [_P, ctypes.POINTER(_I64)]),
     "inr_param_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
     "inr_steps": (_I32, [_P, ctypes.POINTER(_I64)]),
@@ -209,6 +210,10 @@ def inr_create(cfg, block, device=0):
 
 def inr_reset(m, seed):
     _check(_lib.inr_reset(m, seed))
+
+
+def inr_reset_optimizer(m):
+    _check(_lib.inr_reset_optimizer(m))
 
 
 def inr_destroy(m):

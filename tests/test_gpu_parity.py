@@ -588,3 +588,28 @@ def test_stream_ordered_loss_report_matches_fit_report():
         assert row[2] == 0.0
     for m in ms:
         inr.inr_destroy(m)
+
+
+def test_warm_start_keeps_parameters_and_restarts_adam():
+    """inr_reset_optimizer (NEXT-4 warm start): parameters unchanged, Adam
+    moments and the step counter zeroed, so the next step equals a fresh
+    model loaded with those parameters (same seed streams) bitwise."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (32, 32, 32))[0]
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = float(vol.min()), float(vol.max())
+    a = make_gpu_model(blk, 4, reduction=1, **CFG1)
+    inr.inr_fit(a, whole_view(vt), 5, 256, go, stream())
+    p5 = get_params(a)
+    inr.inr_reset_optimizer(a)
+    assert np.array_equal(get_params(a), p5) and inr.inr_steps(a) == 0
+    m, v = inr.inr_get_adam_state(a, np.empty_like(p5), np.empty_like(p5))
+    assert not m.any() and not v.any()
+    b = make_gpu_model(blk, 4, reduction=1, **CFG1)
+    inr.inr_set_params(b, p5)
+    inr.inr_fit(a, whole_view(vt), 2, 256, go, stream())
+    inr.inr_fit(b, whole_view(vt), 2, 256, go, stream())
+    assert np.array_equal(get_params(a), get_params(b))
+    inr.inr_destroy(a)
+    inr.inr_destroy(b)
