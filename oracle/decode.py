@@ -32,9 +32,20 @@ def grid_coords(res):
     return np.stack([x.reshape(-1), y.reshape(-1), z.reshape(-1)], axis=1)
 
 
+def mesh_grid_coords(block, count):
+    """Rectilinear block: the block-normalized coordinates of its first count_d
+    nodes, x_j = fl32((X_{o+j} - P_lo) / (P_hi - P_lo)) (R36), x fastest."""
+    lo, hi = block.physical_box()
+    ax = [((block.mesh[d][block.origin[d]:block.origin[d] + count[d]] - lo[d]) / (hi[d] - lo[d])).astype(np.float32)
+          for d in range(3)]
+    z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+    return np.stack([x.reshape(-1), y.reshape(-1), z.reshape(-1)], axis=1)
+
+
 def decode_grid(model, res, chunk=1 << 16):
-    """Decoded values (R_z, R_y, R_x) float64 in data units, or (R_z, R_y, R_x, D)."""
-    xs = grid_coords(res)
+    """Decoded values (R_z, R_y, R_x) float64 in data units, or (R_z, R_y, R_x, D).
+    A rectilinear model decodes its nodes (res = the node counts, R36)."""
+    xs = grid_coords(res) if model.block.mesh is None else mesh_grid_coords(model.block, res)
     D = model.cfg.out_dim
     out = np.empty((xs.shape[0], D), dtype=np.float64)
     for a in range(0, xs.shape[0], chunk):
@@ -70,8 +81,14 @@ def decode_query(models, p, strict=False):
     for b in np.unique(bid):
         m = models[int(b)]
         sel = bid == b
-        o = m.block.origin.astype(np.float32)
-        x = (p[sel] - o[None, :]) / m.block.n.astype(np.float32)[None, :]
+        if m.block.mesh is None:
+            o = m.block.origin.astype(np.float32)
+            x = (p[sel] - o[None, :]) / m.block.n.astype(np.float32)[None, :]
+        else:   # R36: node index -> physical coordinate -> the block's normalized box
+            lo, hi = m.block.physical_box()
+            P = np.stack([sampler.index_to_physical(m.block.mesh[d], p[sel][:, d].astype(np.float64))
+                          for d in range(3)], axis=1)
+            x = (P - lo[None, :]) / (hi - lo)[None, :]
         y, _ = fit.forward(m, x.astype(np.float32))
         out[sel] = denormalize(y, m.vmin, m.vmax)
     return _channels(out)

@@ -18,12 +18,22 @@ FACE_NAMES = ("-x", "+x", "-y", "+y", "-z", "+z")
 
 
 class Block:
-    """origin (3,) nodes, n (3,) cells per axis, global_dims (3,) nodes; all (x, y, z)."""
+    """origin (3,) nodes, n (3,) cells per axis, global_dims (3,) nodes; all (x, y, z).
+    mesh: None (uniform) or three strictly increasing float64 arrays of the
+    global node coordinates per axis (rectilinear; R36)."""
 
-    def __init__(self, origin, n, global_dims):
+    def __init__(self, origin, n, global_dims, mesh=None):
         self.origin = np.asarray(origin, dtype=np.int64)
         self.n = np.asarray(n, dtype=np.int64)
         self.global_dims = np.asarray(global_dims, dtype=np.int64)
+        self.mesh = None if mesh is None else tuple(np.asarray(m, np.float64) for m in mesh)
+
+    def physical_box(self):
+        """(P_lo, P_hi) of a rectilinear block: the coordinates of nodes o and
+        min(o + n, N - 1) per axis (R36)."""
+        lo = np.array([self.mesh[d][self.origin[d]] for d in range(3)])
+        hi = np.array([self.mesh[d][min(self.origin[d] + self.n[d], self.global_dims[d] - 1)] for d in range(3)])
+        return lo, hi
 
     @property
     def grid(self):
@@ -49,12 +59,12 @@ class Block:
         return out
 
 
-def decompose(global_dims, n):
+def decompose(global_dims, n, mesh=None):
     """All blocks of a volume, in block_id order."""
     gd = np.asarray(global_dims, np.int64)
     n = np.asarray(n, np.int64)
     g = (gd + n - 1) // n
-    return [Block((bx * n[0], by * n[1], bz * n[2]), n, gd)
+    return [Block((bx * n[0], by * n[1], bz * n[2]), n, gd, mesh)
             for bz in range(g[2]) for by in range(g[1]) for bx in range(g[0])]
 
 
@@ -136,11 +146,40 @@ def normalize_values(v, vmin, vmax):
     return t, bool(np.all(const))
 
 
+def physical_to_index(coords, P):
+    """Continuous node index of physical coordinates P on one rectilinear axis:
+    r = i + (P - X_i) / (X_{i+1} - X_i), X_i <= P <= X_{i+1}, i clipped to the
+    mesh's cells, so trilinear in r is trilinear in the physical cell (R36)."""
+    X = np.asarray(coords, np.float64)
+    P = np.asarray(P, np.float64)
+    i = np.clip(np.searchsorted(X, P, side="right") - 1, 0, X.size - 2)
+    return i + (P - X[i]) / (X[i + 1] - X[i])
+
+
+def index_to_physical(coords, r):
+    """The mesh's piecewise-linear map from continuous node index to coordinate."""
+    X = np.asarray(coords, np.float64)
+    r = np.asarray(r, np.float64)
+    i = np.clip(np.floor(r).astype(np.int64), 0, X.size - 2)
+    return X[i] + (r - i) * (X[i + 1] - X[i])
+
+
+def sample_positions(block, x):
+    """Node-index positions r (n, 3) of block-normalized samples x: r = o + x n on a
+    uniform mesh (R5); on a rectilinear mesh the physical point P = P_lo + x (P_hi -
+    P_lo) of the block's box mapped to its continuous index (R36)."""
+    x = np.asarray(x, np.float64)
+    if block.mesh is None:
+        return block.origin[None, :].astype(np.float64) + x * block.n[None, :].astype(np.float64)
+    lo, hi = block.physical_box()
+    P = lo[None, :] + x * (hi - lo)[None, :]
+    return np.stack([physical_to_index(block.mesh[d], P[:, d]) for d in range(3)], axis=1)
+
+
 def targets(volume, block, x, vmin, vmax):
-    """Reference targets at block-normalized x: trilinear at r = o + x n,
-    normalized with the global range (P:L172, P:L205; R5, R7)."""
-    r = block.origin[None, :].astype(np.float64) + np.asarray(x, np.float64) * block.n[None, :].astype(np.float64)
-    return normalize_values(trilinear(volume, r), vmin, vmax)
+    """Reference targets at block-normalized x: trilinear at the sample's node
+    position (R5 / R36), normalized with the global range (P:L172, P:L205; R7)."""
+    return normalize_values(trilinear(volume, sample_positions(block, x)), vmin, vmax)
 
 
 def value_range(volumes):
