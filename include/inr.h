@@ -114,6 +114,18 @@ INR_API inr_status inr_reset(inr_model* m, uint64_t seed);
  * learning-rate schedule restarts), so the next inr_fit continues from the
  * previous timestep's network.  INR_ERR_STATE on a frozen model. */
 INR_API inr_status inr_reset_optimizer(inr_model* m);
+/* Rectilinear mesh (NEXT-4; "for uniform and rectilinear meshes, we
+ * provide a native data sampler") [R36]: coords[d] (host) holds the
+ * N_d strictly increasing physical node coordinates of axis d of the global
+ * volume; the model keeps its block's slice.  From then on the block's network
+ * takes the block-normalized PHYSICAL coordinate x = (P - P_lo)/(P_hi - P_lo),
+ * P_lo/P_hi the coordinates of nodes o and min(o + n, N - 1); fit samples are
+ * uniform in that physical box and their targets trilinear in the physical
+ * cell; inr_decode_grid decodes the block's nodes (res must equal n) and queries
+ * (still global node-index coordinates, routed by R5) are mapped through the
+ * mesh's piecewise-linear node -> coordinate map.  coords NULL restores the
+ * uniform mesh.  Synchronous. */
+INR_API inr_status inr_set_mesh(inr_model* m, const double* const coords[3]);
 /* Free a model (NULL is a no-op).  Models borrowed from a cache must not be destroyed. */
 INR_API inr_status inr_destroy(inr_model* m);
 /* Number of fp32 parameters in the declared order (tables by level, then

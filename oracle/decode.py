@@ -36,8 +36,10 @@ def mesh_grid_coords(block, count):
     """Rectilinear block: the block-normalized coordinates of its first count_d
     nodes, x_j = fl32((X_{o+j} - P_lo) / (P_hi - P_lo)) (R36), x fastest."""
     lo, hi = block.physical_box()
-    ax = [((block.mesh[d][block.origin[d]:block.origin[d] + count[d]] - lo[d]) / (hi[d] - lo[d])).astype(np.float32)
-          for d in range(3)]
+    span = hi - lo
+    # a block one node thick on an axis (span 0) maps that axis to x = 0
+    ax = [(((block.mesh[d][block.origin[d]:block.origin[d] + count[d]] - lo[d]) / span[d]) if span[d] > 0 else
+           np.zeros(count[d])).astype(np.float32) for d in range(3)]
     z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
     return np.stack([x.reshape(-1), y.reshape(-1), z.reshape(-1)], axis=1)
 
@@ -88,7 +90,8 @@ def decode_query(models, p, strict=False):
             lo, hi = m.block.physical_box()
             P = np.stack([sampler.index_to_physical(m.block.mesh[d], p[sel][:, d].astype(np.float64))
                           for d in range(3)], axis=1)
-            x = (P - lo[None, :]) / (hi - lo)[None, :]
+            span = hi - lo
+            x = np.where(span[None, :] > 0, (P - lo[None, :]) / np.where(span > 0, span, 1.0)[None, :], 0.0)
         y, _ = fit.forward(m, x.astype(np.float32))
         out[sel] = denormalize(y, m.vmin, m.vmax)
     return _channels(out)

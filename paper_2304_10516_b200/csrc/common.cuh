@@ -74,7 +74,43 @@ struct ModelDev {
   int faces[6];
   float vmin[kMaxD], vrange[kMaxD], inv_range[kMaxD];   // per-channel normalization (inv_range 0: constant)
   uint32_t k0, k1u, k1b;            // Philox keys (seed_lo, seed_hi ^ 1), (seed_lo, seed_hi ^ 2) [R8]
+  // rectilinear mesh (R36): the block's node coordinates X[o .. o + mesh_n - 1] per axis
+  // (device) and its physical box [plo, plo + pspan]; mesh[0] == null: uniform mesh
+  const double* mesh[3];
+  int mesh_n[3];
+  double plo[3], pspan[3];
 };
+
+// Rectilinear (R36): local cell i (clamped to the block's cells) and fraction of the
+// physical coordinate P on axis d, by binary search over the block's nodes.
+__device__ __forceinline__ int mesh_cell(const ModelDev& md, int d, double P, double& frac) {
+  const double* X = md.mesh[d];
+  const int m = md.mesh_n[d];
+  if (m < 2) { frac = 0.0; return 0; }
+  int lo = 0, hi = m - 1;               // invariant X[lo] <= P < X[hi] (when inside)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (X[mid] <= P) lo = mid; else hi = mid;
+  }
+  frac = __ddiv_rn(__dsub_rn(P, X[lo]), __dsub_rn(X[lo + 1], X[lo]));
+  return lo;
+}
+
+// Rectilinear: block-normalized coordinate of a physical coordinate.
+__device__ __forceinline__ float mesh_x(const ModelDev& md, int d, double P) {
+  return md.pspan[d] > 0.0 ? (float)__ddiv_rn(__dsub_rn(P, md.plo[d]), md.pspan[d]) : 0.f;
+}
+
+// Rectilinear: the physical coordinate of continuous global node index p (float)
+// routed to this block: the mesh's piecewise-linear map on the block's nodes.
+__device__ __forceinline__ double mesh_physical(const ModelDev& md, int d, float p) {
+  const int m = md.mesh_n[d];
+  const double* X = md.mesh[d];
+  if (m < 2) return X[0];
+  const double r = fmin(fmax((double)p - (double)md.o[d], 0.0), (double)(m - 1));
+  const int i = min((int)floor(r), m - 2);
+  return __dadd_rn(X[i], __dmul_rn(__dsub_rn(r, (double)i), __dsub_rn(X[i + 1], X[i])));
+}
 
 // --------------------------------------------------------------- Philox4x32-10
 struct U4 { uint32_t x, y, z, w; };
@@ -122,6 +158,14 @@ __device__ __forceinline__ void sample_target(const ModelDev& md, const float x[
   float f[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
+    if (md.mesh[0]) {   // rectilinear (R36): P = P_lo + x (P_hi - P_lo), located in the block's cells
+      double fr;
+      const int c = mesh_cell(md, d, __dadd_rn(md.plo[d], __dmul_rn((double)x[d], md.pspan[d])), fr);
+      i0[d] = md.o[d] + c;
+      f[d] = fminf(fmaxf((float)fr, 0.f), 1.f);
+      i1[d] = f[d] > 0.f ? i0[d] + 1 : i0[d];
+      continue;
+    }
     float r = __fadd_rn((float)md.o[d], __fmul_rn(x[d], (float)md.n[d]));
     r = fminf(fmaxf(r, 0.f), (float)(md.N[d] - 1));
     float fl = floorf(r);

@@ -179,6 +179,9 @@ struct inr_model {
   int faces[6] = {0, 0, 0, 0, 0, 0};
   float vmin[kMaxD] = {0.f, 0.f, 0.f}, vmax[kMaxD] = {1.f, 1.f, 1.f};   // per-channel range of the last fit
   double last_inv_u = 0.0, last_inv_b = 0.0;   // 1/(B_u D), 1/(B_b D) of the last fit step (report)
+  double* mesh = nullptr;                      // rectilinear (R36): device node coordinates, 3 slices
+  int mesh_n[3] = {0, 0, 0};
+  double plo[3] = {0, 0, 0}, pspan[3] = {0, 0, 0};
   bool frozen = false;       // cache snapshot: parameters only
   bool host_resident = false;
   float* host_params = nullptr;  // pinned copy (host-resident snapshot)
@@ -367,6 +370,55 @@ extern "C" inr_status inr_reset(inr_model* m, uint64_t seed) {
   return INR_OK;
 }
 
+// Rectilinear mesh (NEXT-4; R36): keep the block's slice of the global
+// node coordinates on the device; the fit samples and the decodes go through it.
+static inr_status set_mesh_slices(inr_model* m, const double* const* slices, const int n[3], bool device_src) {
+  const size_t tot = (size_t)n[0] + n[1] + n[2];
+  double* dm = nullptr;
+  CK(cudaSetDevice(m->device));
+  CK(cudaMalloc((void**)&dm, tot * sizeof(double)));
+  size_t off = 0;
+  for (int d = 0; d < 3; ++d) {
+    cudaError_t e = cudaMemcpy(dm + off, slices[d], (size_t)n[d] * sizeof(double),
+                               device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(dm); return cuda_fail(e, "mesh copy"); }
+    off += n[d];
+  }
+  if (m->mesh) cudaFree(m->mesh);
+  m->mesh = dm;
+  for (int d = 0; d < 3; ++d) m->mesh_n[d] = n[d];
+  return INR_OK;
+}
+
+extern "C" inr_status inr_set_mesh(inr_model* m, const double* const coords[3]) {
+  if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
+  if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
+  if (!coords) {   // back to the uniform mesh
+    if (m->mesh) { cudaSetDevice(m->device); cudaFree(m->mesh); }
+    m->mesh = nullptr;
+    return INR_OK;
+  }
+  const double* slices[3];
+  int n[3];
+  double lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    if (!coords[d]) return fail(INR_ERR_INVALID_ARG, "coords[%d] is NULL", d);
+    const int64_t N = m->blk.global_dims[d], o = m->blk.origin[d];
+    for (int64_t i = 0; i + 1 < N; ++i)
+      if (!(coords[d][i + 1] > coords[d][i]))
+        return fail(INR_ERR_INVALID_ARG, "mesh coordinates must be strictly increasing (axis %d)", d);
+    const int64_t last = std::min<int64_t>(o + m->blk.n[d], N - 1);
+    slices[d] = coords[d] + o;
+    n[d] = (int)(last - o + 1);
+    lo[d] = coords[d][o];
+    hi[d] = coords[d][last];
+  }
+  inr_status s = set_mesh_slices(m, slices, n, false);
+  if (s) return s;
+  for (int d = 0; d < 3; ++d) { m->plo[d] = lo[d]; m->pspan[d] = hi[d] - lo[d]; }
+  return INR_OK;
+}
+
 extern "C" inr_status inr_reset_optimizer(inr_model* m) {
   if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
   if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
@@ -382,6 +434,7 @@ extern "C" inr_status inr_destroy(inr_model* m) {
   if (!m) return INR_OK;
   cudaSetDevice(m->device);
   if ((m->host_resident || m->h16) && m->params) cudaFree(m->params);
+  if (m->mesh) cudaFree(m->mesh);
   if (m->mem) cudaFree(m->mem);
   if (m->host_params) cudaFreeHost(m->host_params);
   if (m->h16) { if (m->host_resident) cudaFreeHost(m->h16); else cudaFree(m->h16); }
@@ -467,6 +520,16 @@ static ModelDev model_dev(const inr_model* m) {
   d.block_id = m->block_id;
   d.nfaces = m->nfaces;
   for (int k = 0; k < 6; ++k) d.faces[k] = m->faces[k];
+  if (m->mesh) {
+    size_t off = 0;
+    for (int k = 0; k < 3; ++k) {
+      d.mesh[k] = m->mesh + off;
+      off += (size_t)m->mesh_n[k];
+      d.mesh_n[k] = m->mesh_n[k];
+      d.plo[k] = m->plo[k];
+      d.pspan[k] = m->pspan[k];
+    }
+  }
   for (int c = 0; c < kMaxD; ++c) {
     d.vmin[c] = m->vmin[c];
     d.vrange[c] = m->vmax[c] - m->vmin[c];
@@ -757,6 +820,10 @@ extern "C" inr_status inr_decode_grid_part(const inr_model* m, const int32_t res
   }
   int r[3] = {res[0], res[1], res[2]};
   int c[3] = {count ? count[0] : res[0], count ? count[1] : res[1], count ? count[2] : res[2]};
+  if (m->mesh)
+    for (int d = 0; d < 3; ++d)
+      if (r[d] != m->blk.n[d] || c[d] > m->mesh_n[d])
+        return fail(INR_ERR_INVALID_ARG, "a rectilinear model decodes its nodes: res = n, count <= its node count");
   ModelDev md = model_dev(m);
   {
     ProfScope p(PK_DECODE_GRID, st);
@@ -1039,10 +1106,17 @@ extern "C" inr_status cache_insert(inr_cache* c, int64_t timestep, inr_model* co
     memcpy(m->faces, src->faces, sizeof m->faces);
     memcpy(m->vmin, src->vmin, sizeof m->vmin);
     memcpy(m->vmax, src->vmax, sizeof m->vmax);
+    if (src->mesh) {
+      const double* sl[3] = {src->mesh, src->mesh + src->mesh_n[0], src->mesh + src->mesh_n[0] + src->mesh_n[1]};
+      inr_status ms = set_mesh_slices(m, sl, src->mesh_n, true);
+      if (ms) { delete m; for (auto* x : slot.models) inr_destroy(x); return ms; }
+      memcpy(m->plo, src->plo, sizeof m->plo);
+      memcpy(m->pspan, src->pspan, sizeof m->pspan);
+    }
     m->steps = src->steps;
     m->frozen = true;
     inr_status s = alloc_model(m, true, c->host_resident || c->fp16);
-    if (s) { delete m; for (auto* x : slot.models) inr_destroy(x); return s; }
+    if (s) { inr_destroy(m); for (auto* x : slot.models) inr_destroy(x); return s; }
     m->host_resident = c->host_resident;
     m->staged = false;
     cudaError_t e = cudaSuccess;

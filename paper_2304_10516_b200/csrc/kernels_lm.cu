@@ -188,7 +188,8 @@ __global__ void query_prep_kernel(GroupArgs g, const float* __restrict__ xyz, co
   float x[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d)
-    x[d] = __fdiv_rn(__fsub_rn(__ldg(xyz + 3 * (long long)qi + d), (float)md.o[d]), (float)md.n[d]);
+    x[d] = md.mesh[0] ? mesh_x(md, d, mesh_physical(md, d, __ldg(xyz + 3 * (long long)qi + d)))   // R36
+                      : __fdiv_rn(__fsub_rn(__ldg(xyz + 3 * (long long)qi + d), (float)md.o[d]), (float)md.n[d]);
   qx[j] = make_float4(x[0], x[1], x[2], __int_as_float(slot));
 }
 

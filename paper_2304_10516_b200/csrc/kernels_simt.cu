@@ -303,6 +303,10 @@ __global__ void __launch_bounds__(kTile) decode_grid_simt_kernel(NetDesc net, Mo
     jz = (int)(r / cy);
   }
   float x[3] = {__fdiv_rn((float)jx, (float)rx), __fdiv_rn((float)jy, (float)ry), __fdiv_rn((float)jz, (float)rz)};
+  if (md.mesh[0]) {   // rectilinear (R36): the block's nodes, x_j = fl32((X_{o+j} - P_lo) / (P_hi - P_lo))
+    const int jj[3] = {jx, jy, jz};
+    for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
+  }
   encode_to_smem<F>(net, md.params, x, smem, t);
   float y[kMaxD];
   mlp_forward_simt(net, md.params, smem, t, y);
@@ -350,7 +354,9 @@ __global__ void __launch_bounds__(kTile) decode_query_simt_kernel(QueryArgs qa, 
   int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
   const ModelDev& md = qa.md[slot < 0 ? 0 : slot];
   float x[3];
-  for (int d = 0; d < 3; ++d) x[d] = __fdiv_rn(__fsub_rn(p[d], (float)md.o[d]), (float)md.n[d]);
+  for (int d = 0; d < 3; ++d)
+    x[d] = md.mesh[0] ? mesh_x(md, d, mesh_physical(md, d, p[d]))          // rectilinear (R36)
+                      : __fdiv_rn(__fsub_rn(p[d], (float)md.o[d]), (float)md.n[d]);
   encode_to_smem<F>(qa.net, md.params, x, smem, t);
   float y[kMaxD];
   mlp_forward_simt(qa.net, md.params, smem, t, y);

@@ -609,6 +609,11 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
         x[0] = __fdiv_rn((float)jx, (float)a.res[0]);
         x[1] = __fdiv_rn((float)jy, (float)a.res[1]);
         x[2] = __fdiv_rn((float)jz, (float)a.res[2]);
+        if (md.mesh[0]) {   // rectilinear (R36): the block's nodes
+          const int jj[3] = {jx, jy, jz};
+#pragma unroll
+          for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
+        }
         dst = jx * a.os[0] + jy * a.os[1] + jz * a.os[2];
       }
     } else {

@@ -110,6 +110,7 @@ _SIG = {
     "inr_reset": (_I32, [_P, _U64]),
     "inr_destroy": (_I32, [_P]),
     "inr_reset_optimizer": (_I32, [_P]),
+    "inr_set_mesh": (_I32, [_P, ctypes.POINTER(ctypes.c_void_p)]),
     "inr_param_count": (_I32, [_P, ctypes.POINTER(_I64)]),
     "inr_param_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
     "inr_steps": (_I32, [_P, ctypes.POINTER(_I64)]),
@@ -214,6 +215,17 @@ def inr_reset(m, seed):
 
 def inr_reset_optimizer(m):
     _check(_lib.inr_reset_optimizer(m))
+
+
+def inr_set_mesh(m, coords):
+    """coords: three float64 arrays of the global node coordinates per axis (x, y, z), or None (uniform)."""
+    if coords is None:
+        _check(_lib.inr_set_mesh(m, None))
+        return
+    import numpy as _np
+    arrs = [_np.ascontiguousarray(c, dtype=_np.float64) for c in coords]
+    ptrs = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in arrs])
+    _check(_lib.inr_set_mesh(m, ptrs))
 
 
 def inr_destroy(m):

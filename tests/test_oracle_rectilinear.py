@@ -76,3 +76,14 @@ def test_rectilinear_grid_decode_is_the_node_query():
     q = decode.decode_query(models, pts).reshape(8, 8, 8)
     assert np.allclose(g, q, rtol=0, atol=1e-12)
     assert decode.mesh_grid_coords(b, (9, 1, 1))[-1, 0] == 1.0          # node o + n is x = 1
+
+
+def test_one_node_thick_block_maps_to_x_zero():
+    """N = 17, n = 8: the upper layer o = 16 holds one node; its span is 0 and the
+    axis maps to x = 0 (R36), for grid and query decode alike."""
+    dims = (17, 9, 9)
+    mesh = (stretched(17, 1), stretched(9, 2), stretched(9, 3))
+    b = sampler.decompose(dims, (8, 8, 8), mesh)[2]
+    assert b.origin[0] == 16
+    xs = decode.mesh_grid_coords(b, (1, 2, 2))
+    assert np.all(xs[:, 0] == 0.0) and np.all(np.isfinite(xs))
