@@ -113,6 +113,7 @@ __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
 // samples: float4 (x, y, z, target); writes dfeat fp32 [model][level][Bs][F];
 // adds dW, db into the model's gradient.
 constexpr int kFitThreads = 256;
+constexpr int kDetCtasPerModel = 32;   // deterministic mode: MLP CTAs per model, independent of the group
 
 // Sum 32 per-lane values over the warp; lane l ends with the sum of column l.
 __device__ __forceinline__ float warp_transpose_reduce32(float* v, int lane) {
@@ -498,7 +499,11 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
   const int total = fs.B_u + fs.B_b;
   const int ntiles = (total + kTileM - 1) / kTileM;
   const int slots = 148 * L.ctas_per_sm;
-  int per_model = std::max(1, std::min(ntiles, (slots + nmodels - 1) / nmodels));
+  // CTAs per model: fill the machine; in the deterministic mode a fixed count, so
+  // that the tiles each CTA accumulates in fp32 TMEM (and hence the exact result)
+  // do not depend on how many models share the launch
+  int per_model = fs.det ? std::min(ntiles, kDetCtasPerModel)
+                         : std::max(1, std::min(ntiles, (slots + nmodels - 1) / nmodels));
   dim3 grid(per_model, nmodels);
   float ls = loss_scale_for(fs.B_u);
   switch (g.net.F * 10 + g.net.D) {

@@ -454,10 +454,12 @@ def test_group_fit_matches_single_fits(prec):
     go = inr.inr_fit_opts_default()
     go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
     group = [make_gpu_model(b, 6, reduction=1, precision=prec, **CFG1) for b in blocks]
-    reps = inr.inr_fit_group(group, [whole_view(vt)] * len(group), 6, 256, go, stream())
+    # 8192 + 64 samples = 65 tiles per block: several tiles per MLP CTA, whose order of
+    # fp32 accumulation must not depend on how many models share the launch
+    reps = inr.inr_fit_group(group, [whole_view(vt)] * len(group), 6, 8192, go, stream())
     assert all(r.steps_taken == 6 for r in reps)
     single = make_gpu_model(blocks[6], 6, reduction=1, precision=prec, **CFG1)
-    inr.inr_fit(single, whole_view(vt), 6, 256, go, stream())
+    inr.inr_fit(single, whole_view(vt), 6, 8192, go, stream())
     assert np.array_equal(get_params(single), get_params(group[6]))
     for m in group + [single]:
         inr.inr_destroy(m)
