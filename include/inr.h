@@ -196,7 +196,10 @@ INR_API inr_status inr_fit(inr_model* m, const inr_view* block_values, int32_t s
 /* Same semantics for `nmodels` independent models (one block each, all with the
  * same inr_config and device) in one fused launch per kernel per step
  * (decentralized DNR: no communication between models).  `out`,
- * if non-NULL, is an array of nmodels reports. */
+ * if non-NULL, is an array of nmodels reports.  With PSNR-target stopping each
+ * model leaves the group at the first check where it reaches the target, so it
+ * ends exactly as if fitted alone (report.steps_taken per model) while the
+ * others continue. */
 INR_API inr_status inr_fit_group(inr_model* const* models, const inr_view* views, int32_t nmodels,
                          int32_t steps, int32_t batch, const inr_fit_opts* opts,
                          inr_fit_report* out, cudaStream_t stream);

@@ -632,25 +632,36 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     models[i]->last_inv_u = 1.0 / ((double)batch * D);
     models[i]->last_inv_b = bb > 0 ? 1.0 / ((double)bb * D) : 0.0;
   }
-  const int nchunks = (nmodels + kMaxGroup - 1) / kMaxGroup;
-  std::vector<GroupArgs> groups(nchunks);
-  for (int c = 0; c < nchunks; ++c) {
-    GroupArgs& g = groups[c];
-    memset(&g, 0, sizeof g);
-    g.net = m0->net;
-    g.nmodels = std::min(kMaxGroup, nmodels - c * kMaxGroup);
-    for (int j = 0; j < g.nmodels; ++j) {
-      const inr_model* m = models[c * kMaxGroup + j];
-      const inr_view& v = views[c * kMaxGroup + j];
-      ModelDev& d = g.md[j];
-      d = model_dev(m);
-      d.vbase = v.base;
-      uint32_t k0;
-      philox_key(m->cfg.seed, 1, d.k0, d.k1u);
-      philox_key(m->cfg.seed, 2, k0, d.k1b);
-      for (int k = 0; k < 3; ++k) { d.vlo[k] = v.lo[k]; d.vstride[k] = v.stride[k]; }
+  // the models still training, in chunks of <= 64 per fused launch; with PSNR-target
+  // stopping a model leaves the group at the first check where it reaches the target
+  // (each model stops exactly as if fitted alone; blocks are independent)
+  std::vector<int> active(nmodels);
+  for (int i = 0; i < nmodels; ++i) active[i] = i;
+  std::vector<GroupArgs> groups;
+  int nchunks = 0;
+  auto build_groups = [&]() {
+    nchunks = ((int)active.size() + kMaxGroup - 1) / kMaxGroup;
+    groups.assign(nchunks, GroupArgs());
+    for (int c = 0; c < nchunks; ++c) {
+      GroupArgs& g = groups[c];
+      memset(&g, 0, sizeof g);
+      g.net = m0->net;
+      g.nmodels = std::min(kMaxGroup, (int)active.size() - c * kMaxGroup);
+      for (int j = 0; j < g.nmodels; ++j) {
+        const int i = active[c * kMaxGroup + j];
+        const inr_model* m = models[i];
+        const inr_view& v = views[i];
+        ModelDev& d = g.md[j];
+        d = model_dev(m);
+        d.vbase = v.base;
+        uint32_t k0;
+        philox_key(m->cfg.seed, 1, d.k0, d.k1u);
+        philox_key(m->cfg.seed, 2, k0, d.k1b);
+        for (int k = 0; k < 3; ++k) { d.vlo[k] = v.lo[k]; d.vstride[k] = v.stride[k]; }
+      }
     }
-  }
+  };
+  build_groups();
   // fp16 path: level-major pipeline with a per-call workspace (stream-ordered allocation)
   void* ws_mem = nullptr;
   LmWorkspace ws{};
@@ -684,7 +695,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     ~WsFree() { if (p) cudaFreeAsync(p, s); }
   } ws_free{ws_mem, st};
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = (tc ? 7 : 3) * nchunks;
+  const int launches_per_step = (tc ? 7 : 3) * nchunks;   // (graphs only without probing: fixed groups)
   // CUDA graphs (launch-gap free): without probing, capture one step and replay it
   // per step; while profiling, capture the whole loop (with its event records)
   // once, so per-kernel timings come from the same graph execution.
@@ -704,9 +715,8 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   }
   int taken = 0;
-  bool reached_all = false;
   std::vector<double> psnr(nmodels, 0.0);
-  std::vector<int> reached(nmodels, 0);
+  std::vector<int> reached(nmodels, 0), steps_of(nmodels, -1);
   for (int s = 0; s < steps; ++s) {
     if (exec) {
       if (whole && s > 0) { taken = s + 1; continue; }
@@ -725,20 +735,28 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       for (int c = 0; c < nchunks; ++c) { ProfScope p(PK_PROBE, st); launch_probe(groups[c], groups[c].nmodels, st); }
       CK_LAUNCH("probe");
       CK(cudaStreamSynchronize(st));
-      reached_all = true;
-      for (int i = 0; i < nmodels; ++i) {
+      std::vector<int> still;
+      for (int i : active) {
         double sse = 0;
         CK(cudaMemcpy(&sse, models[i]->acc + 2, sizeof sse, cudaMemcpyDeviceToHost));
         double mse = sse / (32768.0 * D);
         psnr[i] = mse <= 0 ? 200.0 : std::min(200.0, -10.0 * std::log10(mse));
         reached[i] = psnr[i] >= opts->target_psnr;
-        reached_all &= reached[i] != 0;
+        if (reached[i]) steps_of[i] = taken;
+        else still.push_back(i);
       }
-      if (reached_all) break;
+      if (still.empty()) break;
+      if (still.size() != active.size()) {   // the converged models leave the group
+        active.swap(still);
+        build_groups();
+      }
     }
   }
   if (exec) cudaGraphExecDestroy(exec);
-  for (int i = 0; i < nmodels; ++i) models[i]->steps += taken;
+  for (int i = 0; i < nmodels; ++i) {
+    if (steps_of[i] < 0) steps_of[i] = taken;
+    models[i]->steps += steps_of[i];
+  }
   if (!out) return INR_OK;
   CK(cudaStreamSynchronize(st));
   bool nonfinite = false;
@@ -752,7 +770,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     memcpy(acc, tail, sizeof acc);
     memcpy(&flag, tail + 32, sizeof flag);
     inr_fit_report& r = out[i];
-    r.steps_taken = taken;
+    r.steps_taken = steps_of[i];
     r.reached_target = reached[i];
     r.constant_field = all_constant;
     int bb = m->nfaces > 0 ? opts->boundary_batch : 0;

@@ -615,3 +615,29 @@ def test_warm_start_keeps_parameters_and_restarts_adam():
     assert np.array_equal(get_params(a), get_params(b))
     inr.inr_destroy(a)
     inr.inr_destroy(b)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_group_psnr_stopping_is_per_model(prec):
+    """PSNR-target stopping inside a group: each block leaves the group at its own
+    first check above the target (steps differ between blocks) and ends bitwise
+    as if fitted alone with the same options (deterministic mode)."""
+    vol = synth.g2_energy(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
+    go.target_psnr, go.check_interval = 38.0, 10
+    group = [make_gpu_model(b, 8, reduction=1, precision=prec, **CFG1) for b in blocks]
+    reps = inr.inr_fit_group(group, [whole_view(vt)] * len(group), 300, 1024, go, stream())
+    steps = [r.steps_taken for r in reps]
+    print("steps per block", steps, [round(r.probe_psnr, 1) for r in reps])
+    assert len(set(steps)) > 1 and all(r.reached_target for r in reps)
+    for k in (int(np.argmin(steps)), int(np.argmax(steps))):
+        single = make_gpu_model(blocks[k], 8, reduction=1, precision=prec, **CFG1)
+        rep = inr.inr_fit(single, whole_view(vt), 300, 1024, go, stream())
+        assert rep.steps_taken == steps[k] and inr.inr_steps(single) == steps[k]
+        assert np.array_equal(get_params(single), get_params(group[k]))
+        inr.inr_destroy(single)
+    for m in group:
+        inr.inr_destroy(m)
