@@ -126,6 +126,15 @@ INR_API inr_status inr_reset_optimizer(inr_model* m);
  * mesh's piecewise-linear node -> coordinate map.  coords NULL restores the
  * uniform mesh.  Synchronous. */
 INR_API inr_status inr_set_mesh(inr_model* m, const double* const coords[3]);
+/* Model state transfer (NEXT-4 cross-GPU block stealing): the trainable state —
+ * parameters, Adam moments, step counters, value range — as one opaque device
+ * buffer of inr_state_bytes bytes, e.g. to continue a block's fit on another GPU
+ * (the buffer travels by NCCL / peer copy).  Importing into a model of the same
+ * configuration and block makes its next fit steps bitwise those the exporter
+ * would have taken.  Both calls synchronize `stream`. */
+INR_API inr_status inr_state_bytes(const inr_model* m, int64_t* bytes);
+INR_API inr_status inr_export_state(const inr_model* m, void* dst, cudaStream_t stream);
+INR_API inr_status inr_import_state(inr_model* m, const void* src, cudaStream_t stream);
 /* Free a model (NULL is a no-op).  Models borrowed from a cache must not be destroyed. */
 INR_API inr_status inr_destroy(inr_model* m);
 /* Number of fp32 parameters in the declared order (tables by level, then

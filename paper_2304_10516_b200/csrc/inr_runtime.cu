@@ -419,6 +419,69 @@ extern "C" inr_status inr_set_mesh(inr_model* m, const double* const coords[3]) 
   return INR_OK;
 }
 
+// ---- model state transfer (NEXT-4 block stealing): [host meta 256 B][device tail 256 B][params][m][v]
+struct StateMeta {
+  int64_t steps;
+  float vmin[kMaxD], vmax[kMaxD];
+  double last_inv_u, last_inv_b;
+  int64_t P_pad;
+  uint32_t block_id, magic;
+};
+static const uint32_t kStateMagic = 0x494e5253u;
+
+extern "C" inr_status inr_state_bytes(const inr_model* m, int64_t* bytes) {
+  if (!m || !bytes) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  *bytes = 512 + 3 * (int64_t)m->P_pad * 4;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_export_state(const inr_model* m, void* dst, cudaStream_t st) {
+  if (!m || !dst) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (m->frozen) return fail(INR_ERR_STATE, "a frozen cache snapshot has no optimizer state");
+  static thread_local StateMeta meta;   // pinned-free host source: the copy completes before return (sync)
+  memset(&meta, 0, sizeof meta);
+  meta.steps = m->steps;
+  memcpy(meta.vmin, m->vmin, sizeof meta.vmin);
+  memcpy(meta.vmax, m->vmax, sizeof meta.vmax);
+  meta.last_inv_u = m->last_inv_u;
+  meta.last_inv_b = m->last_inv_b;
+  meta.P_pad = m->P_pad;
+  meta.block_id = m->block_id;
+  meta.magic = kStateMagic;
+  char* d = (char*)dst;
+  const size_t n = (size_t)m->P_pad * 4;
+  CK(cudaSetDevice(m->device));
+  CK(cudaMemcpyAsync(d, &meta, sizeof meta, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d + 256, m->step_total, 256, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(d + 512, m->params, n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(d + 512 + n, m->adam_m, 2 * n, cudaMemcpyDeviceToDevice, st));   // m, v contiguous
+  CK(cudaStreamSynchronize(st));
+  return INR_OK;
+}
+
+extern "C" inr_status inr_import_state(inr_model* m, const void* src, cudaStream_t st) {
+  if (!m || !src) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");
+  StateMeta meta;
+  const char* s = (const char*)src;
+  CK(cudaSetDevice(m->device));
+  CK(cudaMemcpyAsync(&meta, s, sizeof meta, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (meta.magic != kStateMagic || meta.P_pad != m->P_pad || meta.block_id != m->block_id)
+    return fail(INR_ERR_INVALID_ARG, "state was exported by a model of another configuration or block");
+  const size_t n = (size_t)m->P_pad * 4;
+  CK(cudaMemcpyAsync(m->step_total, s + 256, 256, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(m->params, s + 512, n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(m->adam_m, s + 512 + n, 2 * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  m->steps = meta.steps;
+  memcpy(m->vmin, meta.vmin, sizeof meta.vmin);
+  memcpy(m->vmax, meta.vmax, sizeof meta.vmax);
+  m->last_inv_u = meta.last_inv_u;
+  m->last_inv_b = meta.last_inv_b;
+  return INR_OK;
+}
+
 extern "C" inr_status inr_reset_optimizer(inr_model* m) {
   if (!m) return fail(INR_ERR_INVALID_ARG, "model is NULL");
   if (m->frozen) return fail(INR_ERR_STATE, "model is a frozen cache snapshot");

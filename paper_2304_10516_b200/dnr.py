@@ -103,6 +103,28 @@ def allgather_metadata(rows):
     return [r for part in out for r in part]
 
 
+def steal_plan(status, already_moved=()):
+    """Block-stealing plan (NEXT-4), identical on every rank: status = [(rank,
+    unfinished blocks)]; each idle rank takes half (at least one, never the last
+    one) of the unfinished blocks of the rank with the most movable ones; a block
+    moves at most once.  Returns [(src, dst, block)]."""
+    rem = {r: list(bl) for r, bl in status}
+    was_moved = set(already_moved)
+    plan = []
+    for idle in sorted(r for r in rem if not rem[r]):
+        movable = {r: [b for b in bl if b not in was_moved] for r, bl in rem.items()}
+        src = max(rem, key=lambda r: (len(movable[r]), -r))
+        if len(rem[src]) < 2 or not movable[src]:
+            break
+        for _ in range(min(len(rem[src]) // 2, len(movable[src]))):
+            b = movable[src].pop()
+            rem[src].remove(b)
+            rem[idle].append(b)
+            was_moved.add(b)
+            plan.append((src, idle, b))
+    return plan
+
+
 def gather_fragments(frag, dst=0):
     """Sort-last exchange: every rank's fragment image [npix][5]
     (C_r, C_g, C_b, A, t_enter) to rank `dst`, stacked [world][npix][5] there
@@ -223,6 +245,127 @@ class DNR:
         rows = [[float(b), float(r.steps_taken), r.loss_uniform, r.loss_boundary, r.probe_psnr]
                 for b, r in zip(self.block_ids, reps)]
         return allgather_metadata(rows)
+
+    def _box(self, b):
+        """Global node box [o, min(o + n, N - 1)] of block b (the view a fit needs, R6)."""
+        o = block_origin(b, self.global_dims, self.n)
+        return o, tuple(min(o[d] + self.n[d], self.global_dims[d] - 1) for d in range(3))
+
+    def fit_to_target(self, local_volume, target_psnr, max_steps, batch, opts, check_interval=50,
+                      round_steps=200, steal=True, stream=0):
+        """Fit every block until its probe PSNR reaches target_psnr or it
+        has taken max_steps, in rounds of round_steps; between rounds, with steal=True,
+        a rank whose blocks have all finished takes over half of the busiest rank's
+        unfinished blocks (NEXT-4 cross-GPU block stealing): the block's training state
+        (inr_export_state: parameters, Adam moments, step counters) and its node box
+        of the volume travel over NCCL (send/recv), and the state returns to its
+        owner at the end.  Blocks are independent and the deterministic
+        mode does not depend on grouping, so the result is the one without stealing,
+        only sooner.  Returns {block: (steps, reached)} for this rank's blocks."""
+        if round_steps % check_interval or max_steps % round_steps:
+            raise ValueError("round_steps must be a multiple of check_interval and divide max_steps")
+        inr = self.inr
+        dist_on = dist.is_available() and dist.is_initialized() and self.world > 1
+        dev = torch.device("cuda", self.device)
+        opts.set_range(self.vmin, self.vmax)
+        opts.target_psnr, opts.check_interval = float(target_psnr), int(check_interval)
+        nz, ny, nx = local_volume.shape[:3]
+        own_view = self.inr.make_view(local_volume.data_ptr(), self.lo, (nx, ny, nz), self._strides(nx, ny), self.D)
+        self._local_volume_for_send = local_volume
+        held = {b: dict(model=m, view=own_view, owner=self.rank, vol=None)
+                for b, m in zip(self.block_ids, self.models)}
+        steps = {b: 0 for b in held}
+        done = {}
+        moved = []                                   # (block, owner, holder) of stolen blocks
+        while True:
+            active = [b for b in held if b not in done and steps[b] < max_steps]
+            if active:
+                reps = inr.inr_fit_group([held[b]["model"] for b in active], [held[b]["view"] for b in active],
+                                         round_steps, batch, opts, stream, True)
+                for b, r in zip(active, reps):
+                    steps[b] += r.steps_taken
+                    if r.reached_target or steps[b] >= max_steps:
+                        done[b] = (steps[b], bool(r.reached_target))
+            remaining = [b for b in held if b not in done]
+            status = [None] * self.world
+            if dist_on:
+                dist.all_gather_object(status, (self.rank, remaining))
+            else:
+                status = [(self.rank, remaining)]
+            if sum(len(r) for _, r in status) == 0:
+                break
+            if not (steal and dist_on):
+                continue
+            plan = steal_plan(status, {b for b, _, _ in moved})
+            for src, dst, b in plan:
+                if self.rank == src:
+                    self._send_block(held.pop(b), b, dst, stream, steps.pop(b))
+                elif self.rank == dst:
+                    owner = next(own for own in range(self.world) if b in partition_blocks(self.nblocks, self.world, own))
+                    held[b], steps[b] = self._recv_block(b, src, owner, stream)
+                moved.append((b, src, dst))
+        # stolen blocks go home: the holder returns the final state to the owner
+        home = {}
+        for b, src, dst in moved:
+            home[b] = dst                            # the last holder
+        for b in sorted(home):
+            owner = next(own for own in range(self.world) if b in partition_blocks(self.nblocks, self.world, own))
+            holder = home[b]
+            if holder == owner:
+                continue
+            if self.rank == holder:
+                e = held.pop(b)
+                self._send_state(e["model"], owner, stream)
+                done_b = done.pop(b)
+                dist.send(torch.tensor([done_b[0], int(done_b[1])], dtype=torch.int64, device=dev), owner)
+                inr.inr_destroy(e["model"])
+            elif self.rank == owner:
+                m = self.models[self.block_ids.index(b)]
+                self._recv_state(m, holder, stream)
+                t = torch.empty(2, dtype=torch.int64, device=dev)
+                dist.recv(t, holder)
+                done[b] = (int(t[0]), bool(t[1]))
+        return {b: done[b] for b in self.block_ids}
+
+    def _send_state(self, m, dst, stream):
+        buf = torch.empty(self.inr.inr_state_bytes(m), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        self.inr.inr_export_state(m, buf.data_ptr(), stream)
+        dist.send(buf, dst)
+
+    def _recv_state(self, m, src, stream):
+        buf = torch.empty(self.inr.inr_state_bytes(m), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        dist.recv(buf, src)
+        torch.cuda.current_stream().synchronize()
+        self.inr.inr_import_state(m, buf.data_ptr(), stream)
+
+    def _send_block(self, entry, b, dst, stream, nsteps):
+        """State, steps taken in this fit and the block's node box of the volume to rank dst."""
+        self._send_state(entry["model"], dst, stream)
+        dist.send(torch.tensor([nsteps], dtype=torch.int64, device=torch.device("cuda", self.device)), dst)
+        o, hi = self._box(b)
+        if entry["vol"] is not None:
+            box = entry["vol"]
+        else:
+            lv = self._local_volume_for_send
+            box = lv[o[2] - self.lo[2]:hi[2] - self.lo[2] + 1, o[1] - self.lo[1]:hi[1] - self.lo[1] + 1,
+                     o[0] - self.lo[0]:hi[0] - self.lo[0] + 1].contiguous()
+        dist.send(box, dst)
+        if entry["model"] not in self.models:        # a block this rank had stolen itself
+            self.inr.inr_destroy(entry["model"])
+
+    def _recv_block(self, b, src, owner, stream):
+        o, hi = self._box(b)
+        m = self.inr.inr_create(self.cfg, self.inr.make_block(o, self.n, self.global_dims), self.device)
+        self._recv_state(m, src, stream)
+        t = torch.empty(1, dtype=torch.int64, device=torch.device("cuda", self.device))
+        dist.recv(t, src)
+        dims = tuple(hi[d] - o[d] + 1 for d in range(3))
+        shape = (dims[2], dims[1], dims[0]) + ((self.D,) if self.D > 1 else ())
+        vol = torch.empty(shape, dtype=torch.float32, device=torch.device("cuda", self.device))
+        dist.recv(vol, src)
+        torch.cuda.current_stream().synchronize()
+        v = self.inr.make_view(vol.data_ptr(), o, dims, self._strides(dims[0], dims[1]), self.D)
+        return dict(model=m, view=v, owner=owner, vol=vol), int(t.item())
 
     def decode_grid_local(self, out, scale=1, ref=None, sse=None, stream=0):
         """Decode every local block at `scale` x resolution into `out`, a tensor

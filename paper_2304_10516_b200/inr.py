@@ -110,6 +110,9 @@ _SIG = {
     "inr_reset": (_I32, [_P, _U64]),
     "inr_destroy": (_I32, [_P]),
     "inr_reset_optimizer": (_I32, [_P]),
+    "inr_state_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "inr_export_state": (_I32, [_P, _P, _P]),
+    "inr_import_state": (_I32, [_P, _P, _P]),
     "inr_set_mesh": (_I32, [_P, ctypes.POINTER(ctypes.c_void_p)]),
     "inr_param_count": (_I32, [_P, ctypes.POINTER(_I64)]),
     "inr_param_bytes": (_I32, [_P, ctypes.POINTER(_I64)]),
@@ -226,6 +229,20 @@ def inr_set_mesh(m, coords):
     arrs = [_np.ascontiguousarray(c, dtype=_np.float64) for c in coords]
     ptrs = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in arrs])
     _check(_lib.inr_set_mesh(m, ptrs))
+
+
+def inr_state_bytes(m):
+    n = _I64()
+    _check(_lib.inr_state_bytes(m, ctypes.byref(n)))
+    return n.value
+
+
+def inr_export_state(m, dst_ptr, stream=0):
+    _check(_lib.inr_export_state(m, dst_ptr, stream))
+
+
+def inr_import_state(m, src_ptr, stream=0):
+    _check(_lib.inr_import_state(m, src_ptr, stream))
 
 
 def inr_destroy(m):

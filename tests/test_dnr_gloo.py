@@ -84,3 +84,12 @@ def test_collectives_world2_gloo():
         assert sse == [1.5, 200.0]
         assert meta == [[0.0, 10.0], [1.0, 11.0]]
         assert mx == 3.0
+
+
+def test_steal_plan():
+    # rank 1 idle takes half of rank 0's six unfinished blocks; rank 2 then takes from the busier of 0 / 1
+    plan = dnr.steal_plan([(0, [0, 1, 2, 3, 4, 5]), (1, []), (2, [])])
+    assert plan == [(0, 1, 5), (0, 1, 4), (0, 1, 3), (0, 2, 2)]
+    assert dnr.steal_plan([(0, [7]), (1, [])]) == []                  # never the last block
+    assert dnr.steal_plan([(0, [1, 2]), (1, [])], already_moved={1, 2}) == []   # a block moves once
+    assert dnr.steal_plan([(0, [1, 2]), (1, [3])]) == []              # nobody idle
