@@ -78,8 +78,8 @@ def oracle_step_sample(steps, warmup, frac=0.25):
             o_fit.train_step(m, vol, opts, bu)
         dt = time.perf_counter() - t0
     coords = steps * (bu + bb)
-    desc = (f"{steps} oracle fit steps of one 128^3 cfg2 block at {bu}+{bb} coords/step "
-            f"(1/{int(8 / frac)} of a cfg2 step), numpy fp64, 1 thread")
+    desc = (f"{steps} oracle fit steps (after {warmup} warm-up) of one 128^3 cfg2 block at {bu}+{bb} "
+            f"coords/step ({frac / 8:.4f} of a cfg2 step), numpy fp64, 1 thread")
     return coords / dt, 1, desc
 
 
@@ -87,8 +87,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps, warm = max(1, args.steps), max(0, min(args.warmup, 1))
-    v, cores, desc = oracle_step_sample(steps, warm)
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    # each step a bounded sample of one cfg2 block-step, sized so that the whole
+    # K + W run stays within ~2 minutes (the oracle does ~15 K coords/s on one core)
+    frac = max(1.0 / 64, min(0.25, 15000.0 * 120.0 / (steps + warm) / (B_U + B_B)))
+    v, cores, desc = oracle_step_sample(steps, warm, frac)
     line = {
         "metric": "fit_coords_per_s", "value": v, "unit": "coords/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
