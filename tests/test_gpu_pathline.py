@@ -123,6 +123,54 @@ def test_decode_grid_part_ragged_upper_block():
     inr.inr_destroy(m)
 
 
+@pytest.mark.parametrize("flags", [inr.CACHE_FP16 | inr.CACHE_HOST_RESIDENT, inr.CACHE_HOST_RESIDENT])
+def test_pathlines_from_host_and_fp16_caches(flags):
+    """inr_pathlines over a pinned-host / fp16 window equals decoding every
+    element (staged the same way) and tracing on the GPU, bitwise."""
+    n, nb = 33, 16
+    steps = [3, 4, 5]
+    W = _tgv_window(n, [0.25 * s for s in steps])
+    blocks = sampler.decompose((n, n, n), (nb, nb, nb))
+    cache = inr.cache_create(4, flags)
+    for ts, vol in zip(steps, W):
+        vt = gpu_volume(vol)
+        lo, hi = sampler.value_range([vol])
+        go = inr.inr_fit_opts_default()
+        go.set_range(lo, hi)
+        ms = []
+        for b in blocks:
+            m = make_gpu_model(b, 7, precision=1, **V)
+            inr.inr_fit(m, whole_view(vt), 20, 1024, go, stream())
+            ms.append(m)
+        inr.cache_insert(cache, ts, ms, stream())
+        for m in ms:
+            inr.inr_destroy(m)
+    seeds = _seeds(n, 64, np.random.default_rng(9))
+    M, K = seeds.shape[0], 100
+    sd = torch.from_numpy(seeds).cuda()
+    vert = torch.full((M, K + 1, 5), float("nan"), dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(M, dtype=torch.int32, device="cuda")
+    why = torch.zeros(M, dtype=torch.int32, device="cuda")
+    inr.inr_pathlines(cache, inr.INR_WINDOW_REVERSE | inr.INR_WINDOW_NEGATE, sd.data_ptr(), M, 0.05, K,
+                      vert.data_ptr(), cnt.data_ptr(), why.data_ptr(), stream())
+    torch.cuda.synchronize()
+    gpu = (vert.cpu().numpy(), cnt.cpu().numpy(), why.cpu().numpy())
+    dec = []
+    for i in range(len(steps)):
+        _, ms = inr.cache_get(cache, i)
+        g = torch.empty((n, n, n, 3), device="cuda")
+        for m, b in zip(ms, blocks):
+            o = b.origin
+            c = tuple(min(nb, n - o[d]) for d in range(3))
+            inr.inr_decode_grid(m, (nb, nb, nb), g[o[2]:, o[1]:, o[0]:].data_ptr(), (3, 3 * n, 3 * n * n), None,
+                                None, stream(), count=c)
+        torch.cuda.synchronize()
+        dec.append(g.cpu().numpy())
+    rg, rt, sgn = o_pl.reverse_negate(dec, [float(s) for s in steps], reverse=True, negate=True)
+    _assert_same(gpu, _gpu_trace(rg, rt, (n, n, n), sgn, seeds, 0.05, K))
+    inr.cache_destroy(cache)
+
+
 def test_pathlines_over_cached_window():
     """Backward tracing P = pathline(negate(reverse(W))) over four
     cached timesteps of fitted D = 3 block models (27 blocks, ragged)."""

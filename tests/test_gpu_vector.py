@@ -10,8 +10,8 @@ from oracle import decode as o_decode, fit as o_fit, sampler
 from oracle.model import InrModel, init_params
 from paper_2304_10516_b200 import inr
 
-from gpu_util import gpu_volume, get_grads, make_gpu_model, normwise, oracle_config, per_tensor_rel, stream, \
-    whole_view
+from gpu_util import gpu_volume, get_grads, get_params, make_gpu_model, normwise, oracle_config, per_tensor_rel, \
+    stream, whole_view
 from test_gpu_parity import _perturbed_params, componentwise_ratio, gradient_abs_bound, linear_regime
 
 pytestmark = pytest.mark.gpu
@@ -174,3 +174,28 @@ def test_replica_channels_match_scalar_model_bitwise():
             assert torch.equal(o3[..., c], o1), (prec, c)
         inr.inr_destroy(m1)
         inr.inr_destroy(m3)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_vector_deterministic_and_grouping_independent(prec):
+    """D = 3 in the deterministic mode: two runs are bitwise equal, and a block
+    fitted in a group equals the same block fitted alone (65 tiles per block)."""
+    vol = tgv(32)
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    lo, hi = sampler.value_range([vol])
+    go = inr.inr_fit_opts_default()
+    go.set_range(lo, hi)
+    go.boundary_batch = 64
+    vt = gpu_volume(vol)
+    runs = []
+    for _ in range(2):
+        group = [make_gpu_model(b, 4, reduction=1, precision=prec, **V1) for b in blocks]
+        inr.inr_fit_group(group, [whole_view(vt)] * len(group), 4, 8192, go, stream())
+        runs.append([get_params(m) for m in group])
+        for m in group:
+            inr.inr_destroy(m)
+    assert all(np.array_equal(a, b) for a, b in zip(*runs))
+    single = make_gpu_model(blocks[3], 4, reduction=1, precision=prec, **V1)
+    inr.inr_fit(single, whole_view(vt), 4, 8192, go, stream())
+    assert np.array_equal(get_params(single), runs[0][3])
+    inr.inr_destroy(single)
