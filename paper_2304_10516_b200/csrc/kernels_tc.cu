@@ -576,9 +576,9 @@ __global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, Fw
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
   uint32_t phase = 0, img_phase = 0, feat_phase = 0;
   int cur = -1;  // model whose weight image is in smem
-  // tiles are visited grid-stride: the CTAs in flight work on consecutive tiles,
-  // i.e. (MODE 2, tiles grouped by block) on one or two blocks' tables at a time;
-  // a CTA reloads weights only when its next tile belongs to another block
+  // tiles are visited grid-stride: the CTAs in flight work on consecutive tiles
+  // (MODE 3: tiles grouped by block, so one or two blocks' weights at a time); a
+  // CTA reloads the weight image only when its next tile belongs to another block
   long long t0 = blockIdx.x, t1;
   if constexpr (MODE == 0) t1 = (a.q + kTileM - 1) / kTileM;
   else if constexpr (MODE == 1) t1 = ((long long)a.cnt[0] * a.cnt[1] * a.cnt[2] + kTileM - 1) / kTileM;
