@@ -400,7 +400,20 @@ def run_ours(args):
         torch.cuda.synchronize()
         decode["gather_ms"] = dnr.allreduce_max((time.perf_counter() - t0) * 1e3)
         decode["gather_bytes"] = int(4 * SIDE ** 3 * world)
-        del full
+        # the same gather fused into the decode: every rank's decode kernels store their
+        # slab into rank 0's volume through NVLink peer memory (CUDA IPC)
+        target = d.peer_volume(0)                # rank 0's volume, mapped once on every rank (CUDA IPC)
+        d.decode_to_rank(target, stream)         # warm
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        p2p = d.decode_to_rank(target, stream)
+        torch.cuda.synchronize()
+        decode["decode_and_gather_p2p_ms"] = dnr.allreduce_max((time.perf_counter() - t0) * 1e3)
+        decode["decode_then_nccl_gather_ms"] = dec_ms + decode["gather_ms"]
+        if rank == 0:
+            decode["p2p_equals_nccl_gather"] = bool(torch.equal(p2p, full))
+        del full, p2p, target
     done = args.warmup + args.steps + e_steps
     if args.psnr_steps > done:
         d.fit(vol, args.psnr_steps - done, B_U, opts, stream, report=True)

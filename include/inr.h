@@ -372,6 +372,17 @@ INR_API inr_status inr_render_stats(const inr_renderer* r, int64_t* evaluated, i
 INR_API inr_status inr_composite(const float* fragments, int32_t nfrag, int64_t npixels, const float bg[3],
                          float* image, cudaStream_t stream);
 
+/* ---- peer memory (a18 fused with the decode over NVLink) ----
+ * inr_ipc_handle: the CUDA IPC handle (64 bytes) of the allocation holding the
+ * device pointer ptr and ptr's offset in it; inr_ipc_open (in another process):
+ * maps it on `device` with peer access (*ptr = mapping + offset; *base for
+ * inr_ipc_close).  With it every rank decodes its blocks straight into rank 0's
+ * global volume (inr_decode_grid with out = the peer pointer): the decode
+ * kernels' stores are the gather. */
+INR_API inr_status inr_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset);
+INR_API inr_status inr_ipc_open(const unsigned char handle[64], int64_t offset, int device, void** ptr, void** base);
+INR_API inr_status inr_ipc_close(void* base);
+
 /* ---- parity / test surface ---- */
 /* Copy n = inr_param_count floats of parameters / last-step gradients / Adam m /
  * Adam v in the declared order (synchronous). */

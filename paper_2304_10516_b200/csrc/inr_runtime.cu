@@ -4,6 +4,7 @@
 // allocation per model), builds the per-group kernel parameter blocks, runs the
 // fit loop (optionally as a replayed CUDA graph per step), dispatches decode,
 // and implements the FIFO timestep window.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1605,3 +1606,52 @@ extern "C" inr_status inr_composite(const float* frags, int32_t nfrag, int64_t n
   CK_LAUNCH("composite");
   return INR_OK;
 }
+
+// ------------------------------------------------------------ peer memory
+// Fused decode + gather over NVLink (a18): a rank exports the allocation behind a
+// device pointer as a CUDA IPC handle, the other ranks open it and the decode
+// kernels store their slabs straight into the destination through peer memory.
+extern "C" inr_status inr_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  // the allocation's base: a driver-API query, resolved at run time (no link-time libcuda)
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(INR_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    get_range = (GetRange)fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return fail(INR_ERR_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void*)base));
+  static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &h, 64);
+  *offset = (int64_t)((CUdeviceptr)ptr - base);
+  return INR_OK;
+}
+
+extern "C" inr_status inr_ipc_open(const unsigned char handle[64], int64_t offset, int device, void** ptr,
+                                   void** base) {
+  if (!handle || !ptr || !base) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  CK(cudaSetDevice(device));
+  void* b = nullptr;
+  CK(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = b;
+  *ptr = (char*)b + offset;
+  return INR_OK;
+}
+
+extern "C" inr_status inr_ipc_close(void* base) {
+  if (!base) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  CK(cudaIpcCloseMemHandle(base));
+  return INR_OK;
+}
+

@@ -367,12 +367,18 @@ class DNR:
         v = self.inr.make_view(vol.data_ptr(), o, dims, self._strides(dims[0], dims[1]), self.D)
         return dict(model=m, view=v, owner=owner, vol=vol), int(t.item())
 
-    def decode_grid_local(self, out, scale=1, ref=None, sse=None, stream=0):
+    def decode_grid_local(self, out, scale=1, ref=None, sse=None, stream=0, global_strides=False):
         """Decode every local block at `scale` x resolution into `out`, a tensor
         [z, y, x] covering the local cores at that resolution (strided writes,
         no copies); optional fused SSE against `ref` (same layout).  Vector
-        fields: out is [z, y, x, c]."""
-        nz, ny, nx = out.shape[:3]
+        fields: out is [z, y, x, c].  global_strides: out is (a view or a device
+        pointer at this rank's lo corner of) the global volume's layout."""
+        if global_strides:
+            nx, ny = self.global_dims[0], self.global_dims[1]
+            base_ptr = out if isinstance(out, int) else out.data_ptr()
+        else:
+            nz, ny, nx = out.shape[:3]
+            base_ptr = out.data_ptr()
         res = tuple(int(b * scale) for b in self.n)
         for b, m in zip(self.block_ids, self.models):
             o = block_origin(b, self.global_dims, self.n)
@@ -380,10 +386,11 @@ class DNR:
             # a block at the upper domain face decodes only the lattice points up to N (R19):
             # the first (N - o) * scale points of its res-point lattice
             cnt = tuple(min(res[d], (self.global_dims[d] - o[d]) * scale) for d in range(3))
-            base = out[off[2]:, off[1]:, off[0]:]
+            st = self._strides(nx, ny)
+            ptr = base_ptr + 4 * (off[0] * st[0] + off[1] * st[1] + off[2] * st[2])
             refp = ref[off[2]:, off[1]:, off[0]:].data_ptr() if ref is not None else None
-            self.inr.inr_decode_grid(m, res, base.data_ptr(), self._strides(nx, ny), refp,
-                                     sse.data_ptr() if sse is not None else None, stream, count=cnt)
+            self.inr.inr_decode_grid(m, res, ptr, st, refp, sse.data_ptr() if sse is not None else None, stream,
+                                     count=cnt)
 
     def render(self, cam, tf, step, background=(0.0, 0.0, 0.0), stop_alpha=0.99, cells=16, use_macrocells=True,
                stream=0, dst=0):
@@ -410,6 +417,38 @@ class DNR:
         self.inr.inr_composite(frags.data_ptr(), frags.shape[0], npix, background, img.data_ptr(), stream)
         return img
 
+    def peer_volume(self, dst=0):
+        """Collective: rank `dst` allocates the global [z][y][x] volume and every
+        other rank maps it through NVLink peer memory (CUDA IPC, once).  Returns
+        (tensor on dst / None, device pointer of the volume on this rank)."""
+        dev = torch.device("cuda", self.device)
+        gx, gy, gz = self.global_dims
+        full = torch.empty((gz, gy, gx) + ((self.D,) if self.D > 1 else ()), dtype=torch.float32,
+                           device=dev) if self.rank == dst else None
+        if not (dist.is_available() and dist.is_initialized() and self.world > 1):
+            return full, full.data_ptr()
+        meta = [None] * self.world
+        dist.all_gather_object(meta, self.inr.inr_ipc_handle(full.data_ptr()) if self.rank == dst else None)
+        if self.rank == dst:
+            return full, full.data_ptr()
+        ptr, base = self.inr.inr_ipc_open(meta[dst][0], meta[dst][1], self.device)
+        self._peer_bases = getattr(self, "_peer_bases", []) + [base]
+        return None, ptr
+
+    def decode_to_rank(self, target, stream=0):
+        """Decode every rank's blocks (1x) straight into the global volume of
+        peer_volume() (a18 fused with the decode): the decode kernels store each
+        rank's slab through peer memory; a barrier ends it.  No staging copy, no
+        NCCL transfer of the slabs."""
+        _, ptr = target
+        gx, gy = self.global_dims[0], self.global_dims[1]
+        corner = ptr + 4 * self.D * (self.lo[0] + gx * (self.lo[1] + gy * self.lo[2]))
+        self.decode_grid_local(corner, 1, None, None, stream, global_strides=True)
+        torch.cuda.current_stream().synchronize()
+        if dist.is_available() and dist.is_initialized() and self.world > 1:
+            dist.barrier()
+        return target[0]
+
     def core_box(self):
         """(lo, hi inclusive) of this rank's core nodes (the ghost layer excluded)."""
         hi = [h if h == self.global_dims[d] - 1 else h - 1 for d, h in enumerate(self.hi)]
@@ -429,6 +468,9 @@ class DNR:
         return sum(self.inr.inr_param_bytes(m) for m in self.models)
 
     def close(self):
+        for base in getattr(self, "_peer_bases", []):
+            self.inr.inr_ipc_close(base)
+        self._peer_bases = []
         for m in self.models:
             self.inr.inr_destroy(m)
         self.models = []

@@ -147,6 +147,9 @@ _SIG = {
                           ctypes.c_double, _I32, _P, _P]),
     "inr_render_stats": (_I32, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
     "inr_composite": (_I32, [_P, _I32, _I64, ctypes.POINTER(ctypes.c_float), _P, _P]),
+    "inr_ipc_handle": (_I32, [_P, ctypes.c_char_p, ctypes.POINTER(_I64)]),
+    "inr_ipc_open": (_I32, [ctypes.c_char_p, _I64, ctypes.c_int, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "inr_ipc_close": (_I32, [_P]),
     "inr_get_params": (_I32, [_P, _P, _I64]),
     "inr_set_params": (_I32, [_P, _P, _I64]),
     "inr_get_grads": (_I32, [_P, _P, _I64]),
@@ -354,6 +357,26 @@ def inr_render_stats(r):
 
 def inr_composite(frag_ptr, nfrag, npixels, bg, img_ptr, stream=0):
     _check(_lib.inr_composite(frag_ptr, nfrag, npixels, (ctypes.c_float * 3)(*bg), img_ptr, stream))
+
+
+# ---- peer memory (fused decode + gather)
+def inr_ipc_handle(ptr):
+    """(64-byte handle, offset) of the device allocation holding ptr."""
+    h = ctypes.create_string_buffer(64)
+    off = _I64()
+    _check(_lib.inr_ipc_handle(ptr, h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+def inr_ipc_open(handle, offset, device):
+    """Map another process's allocation: (pointer, base for inr_ipc_close)."""
+    p, b = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(_lib.inr_ipc_open(handle, offset, device, ctypes.byref(p), ctypes.byref(b)))
+    return p.value, b.value
+
+
+def inr_ipc_close(base):
+    _check(_lib.inr_ipc_close(base))
 
 
 # ---- cache

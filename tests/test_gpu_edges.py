@@ -116,3 +116,22 @@ def test_one_pixel_render_and_miss(models):
     f = frag.cpu().numpy()[0]
     assert np.all(f[:4] == 0) and np.isinf(f[4])
     inr.inr_renderer_destroy(r)
+
+
+def test_decode_to_rank_single_process_matches_local_decode():
+    """DNR.decode_to_rank without a process group: the global volume equals the
+    local decode (the peer-memory path is exercised by bench.py at N > 1)."""
+    from paper_2304_10516_b200 import dnr
+    vol = torch.from_numpy(synth.g1_analytic(32).numpy()).cuda()
+    d = dnr.DNR((32, 32, 32), (16, 16, 16), inr.make_config(precision=1, **NET))
+    d.value_range(vol, stream())
+    go = inr.inr_fit_opts_default()
+    d.fit(vol, 10, 256, go, stream(), report=False)
+    a = torch.empty_like(vol)
+    d.decode_grid_local(a, 1, None, None, stream())
+    b = d.decode_to_rank(d.peer_volume(0), stream())
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    h, off = inr.inr_ipc_handle(b[3:].data_ptr())
+    assert len(h) == 64 and off >= 3 * 32 * 32 * 4
+    d.close()
