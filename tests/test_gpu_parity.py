@@ -30,7 +30,8 @@ def test_init_bitwise(kw):
 
 
 @pytest.mark.parametrize("kw", [CFG1, CFG2, dict(levels=8, features=8, log2_table_size=16, mlp_hidden_layers=1),
-                                dict(levels=12, features=1, log2_table_size=12, mlp_hidden_layers=1)])
+                                dict(levels=12, features=1, log2_table_size=12, mlp_hidden_layers=1),
+                                dict(CFG2, log2_table_size=22)])                  # cfg5's table size
 def test_encode_indices_bitexact_features_1e5(kw):
     blk = sampler.decompose((64, 64, 64), (64, 64, 64))[0]
     m = make_gpu_model(blk, 3, **kw)
