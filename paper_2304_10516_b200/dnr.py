@@ -10,7 +10,13 @@ tests) is used only for the few reductions the method needs:
   * before fitting: all-reduce MIN / MAX of the value range
   * after fitting:  all-gather of per-block metadata
   * after decoding: all-reduce SUM of the squared error -> PSNR
-  * optionally:     gather of decoded slabs to rank 0
+  * optionally:     gather of decoded slabs to rank 0,
+                    or the decode storing them into rank 0's volume through
+                    NVLink peer memory (peer_volume / decode_to_rank)
+and for the consumers and training variants:
+  * render:         gather of sort-last fragments to rank 0
+  * fit_to_target:  per-round all-gather of unfinished blocks and send/recv
+                    of stolen blocks' training state            (NEXT-4)
 
 Nothing is communicated inside the fit loop.  All numerical work runs in
 libinr.so (paper_2304_10516_b200.inr); this module only marshals views and
