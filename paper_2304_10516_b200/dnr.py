@@ -111,18 +111,22 @@ def allgather_metadata(rows):
 
 def steal_plan(status, already_moved=()):
     """Block-stealing plan (NEXT-4), identical on every rank: status = [(rank,
-    unfinished blocks)]; each idle rank takes half (at least one, never the last
-    one) of the unfinished blocks of the rank with the most movable ones; a block
-    moves at most once.  Returns [(src, dst, block)]."""
+    unfinished blocks)]; each idle rank in turn takes an even share (at least
+    one, never the last one) of the unfinished blocks of the rank with the most
+    movable ones, so one busy rank's blocks spread over it and all idle ranks; a
+    block moves at most once.  Returns [(src, dst, block)]."""
     rem = {r: list(bl) for r, bl in status}
     was_moved = set(already_moved)
     plan = []
-    for idle in sorted(r for r in rem if not rem[r]):
+    idle_ranks = sorted(r for r in rem if not rem[r])
+    for i, idle in enumerate(idle_ranks):
         movable = {r: [b for b in bl if b not in was_moved] for r, bl in rem.items()}
         src = max(rem, key=lambda r: (len(movable[r]), -r))
         if len(rem[src]) < 2 or not movable[src]:
             break
-        for _ in range(min(len(rem[src]) // 2, len(movable[src]))):
+        # share the source's blocks evenly with it and the idle ranks still to serve
+        share = max(1, len(rem[src]) // (len(idle_ranks) - i + 1))
+        for _ in range(min(share, len(movable[src]))):
             b = movable[src].pop()
             rem[src].remove(b)
             rem[idle].append(b)
@@ -261,8 +265,8 @@ class DNR:
                       round_steps=200, steal=True, stream=0):
         """Fit every block until its probe PSNR reaches target_psnr or it
         has taken max_steps, in rounds of round_steps; between rounds, with steal=True,
-        a rank whose blocks have all finished takes over half of the busiest rank's
-        unfinished blocks (NEXT-4 cross-GPU block stealing): the block's training state
+        ranks whose blocks have all finished take over an even share of the busiest
+        rank's unfinished blocks (NEXT-4 cross-GPU block stealing): the block's training state
         (inr_export_state: parameters, Adam moments, step counters) and its node box
         of the volume travel over NCCL (send/recv), and the state returns to its
         owner at the end.  Blocks are independent and the deterministic

@@ -87,9 +87,12 @@ def test_collectives_world2_gloo():
 
 
 def test_steal_plan():
-    # rank 1 idle takes half of rank 0's six unfinished blocks; rank 2 then takes from the busier of 0 / 1
+    # ranks 1 and 2 idle: rank 0's six unfinished blocks end up two per rank
     plan = dnr.steal_plan([(0, [0, 1, 2, 3, 4, 5]), (1, []), (2, [])])
-    assert plan == [(0, 1, 5), (0, 1, 4), (0, 1, 3), (0, 2, 2)]
+    assert plan == [(0, 1, 5), (0, 1, 4), (0, 2, 3), (0, 2, 2)]
+    # eight blocks, three idle ranks: 2 + 2 + 2 + 2
+    plan = dnr.steal_plan([(0, list(range(8))), (1, []), (2, []), (3, [])])
+    assert [sum(1 for p in plan if p[1] == r) for r in (1, 2, 3)] == [2, 2, 2]
     assert dnr.steal_plan([(0, [7]), (1, [])]) == []                  # never the last block
     assert dnr.steal_plan([(0, [1, 2]), (1, [])], already_moved={1, 2}) == []   # a block moves once
     assert dnr.steal_plan([(0, [1, 2]), (1, [3])]) == []              # nobody idle
