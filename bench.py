@@ -426,6 +426,8 @@ def run_ours(args):
     for dd in range(3):
         ncore *= (d.hi[dd] - d.lo[dd] + 1) if d.hi[dd] == gdims[dd] - 1 else (d.hi[dd] - d.lo[dd])
     psnr = d.psnr(float(sse.item()), ncore)
+    bp = d.block_psnrs(vol, stream)
+    psnr_block_min = dnr.allreduce_max(-min(bp.values())) * -1.0
     raw_bytes = 4.0 * SIDE ** 3
     ratio = raw_bytes / d.param_bytes()
 
@@ -468,7 +470,8 @@ def run_ours(args):
             "dtype": "f16-mlp/f32" if prec else "f32", "data": "synthetic",
             "config": workload_config(world, args),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "decode": decode, "render": render, "psnr_db": psnr, "psnr_after_steps": done,
+            "decode": decode, "render": render, "psnr_db": psnr, "psnr_block_min_db": psnr_block_min,
+            "psnr_after_steps": done,
             "compression_ratio": ratio,
             "clocks": clk, "gpu_launches": launches,
         }

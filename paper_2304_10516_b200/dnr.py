@@ -470,6 +470,26 @@ class DNR:
         core = local_out[: hi[2] - lo[2] + 1, : hi[1] - lo[1] + 1, : hi[0] - lo[0] + 1].contiguous()
         return gather_slabs(core, lo, self.global_dims, dst)
 
+    def block_psnrs(self, local_volume, stream=0):
+        """PSNR of every local block on its own core nodes (1x decode against the
+        volume, fused SSE per block): {block_id: dB}."""
+        out = torch.empty_like(local_volume)
+        sse = torch.zeros(len(self.models), dtype=torch.float64, device=local_volume.device)
+        nz, ny, nx = local_volume.shape[:3]
+        st = self._strides(nx, ny)
+        res = tuple(self.n)
+        cores = []
+        for j, (b, m) in enumerate(zip(self.block_ids, self.models)):
+            o = block_origin(b, self.global_dims, self.n)
+            off = [o[d] - self.lo[d] for d in range(3)]
+            cnt = tuple(min(res[d], self.global_dims[d] - o[d]) for d in range(3))
+            ptr = 4 * (off[0] * st[0] + off[1] * st[1] + off[2] * st[2])
+            self.inr.inr_decode_grid(m, res, out.data_ptr() + ptr, st, local_volume.data_ptr() + ptr,
+                                     sse.data_ptr() + 8 * j, stream, count=cnt)
+            cores.append(cnt[0] * cnt[1] * cnt[2] * self.D)
+        torch.cuda.current_stream().synchronize()
+        return {b: psnr_from_sse(float(e), c) for b, e, c in zip(self.block_ids, sse.tolist(), cores)}
+
     def psnr(self, sse_local, count_local):
         sse, cnt = allreduce_sum([sse_local, count_local])
         return psnr_from_sse(sse, cnt)
