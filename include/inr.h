@@ -3,7 +3,7 @@
  *
  * The operation is the hot path of arXiv 2304.10516 ("distributed neural
  * representation", DNR): one implicit neural representation per spatial block
- * of a scalar volume,
+ * of a scalar (or vector, D = 3) volume,
  *     Phi : R^3 -> R^D, (x,y,z) -> v                    (Eq. 1)
  * built from a multiresolution hash-grid encoding and a small ReLU MLP
  * (PAPER.md L157-158, L217-218), fitted to uniformly sampled, interpolated and
@@ -11,8 +11,11 @@
  *     L = (1 - lambda) L1(X_Uniform, Y_Uniform) + lambda L1(X_Bound, Y_Bound)
  * (Eq. 2) and Adam with a step learning-rate schedule (L220), then
  * decoded by coordinate query or to a grid (L175-176, L268), and cached in a
- * FIFO window of timesteps (L238, L271-274, L290).  Where the paper is silent
- * the readings R1..R25 of DESIGN.md apply; they are cited below as [Rn].
+ * FIFO window of timesteps (L238, L271-274, L290); plus the paper's consumers
+ * of that window — backward pathlines (L411-424) and direct-query volume
+ * rendering (L268, L293-300) — and the multi-GPU plumbing around them.  Where
+ * the paper is silent the readings R1..R36 of DESIGN.md apply; they are cited
+ * below as [Rn].
  *
  * Conventions
  *  - Every function returns an inr_status and never aborts or throws.  On a
@@ -26,7 +29,8 @@
  *  - Coordinates are (x, y, z); volumes are x-fastest, then y, then z.
  *  - A block with core origin o and n cells per axis maps node position p to
  *    the block-normalized x = (p - o)/n in [0,1]^3 (cell-span convention, so
- *    neighbouring blocks share the face plane o + n) [R5].
+ *    neighbouring blocks share the face plane o + n) [R5]; on a rectilinear
+ *    mesh (inr_set_mesh) through the node coordinates instead [R36].
  *  - Sticky CUDA errors surface as INR_ERR_CUDA at the next call.
  *  - There is no CPU fallback: without a usable sm_100 device every call that
  *    needs one fails with INR_ERR_CUDA.
