@@ -135,3 +135,35 @@ def test_decode_to_rank_single_process_matches_local_decode():
     h, off = inr.inr_ipc_handle(b[3:].data_ptr())
     assert len(h) == 64 and off >= 3 * 32 * 32 * 4
     d.close()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_nonfinite_loss_and_parameters_are_reported(prec):
+    """a non-finite loss or parameter after a step is an error
+    (INR_ERR_NONFINITE) of the synchronous report and flag 1 of inr_fit_losses."""
+    blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
+    vol = synth.g1_analytic(16).numpy().copy()
+    vol[5:11, 5:11, 5:11] = np.inf                        # targets become non-finite
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = 0.0, 1.0
+    m = make_gpu_model(blk, 1, precision=prec, **NET)
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_fit(m, whole_view(vt), 2, 512, go, stream())
+    assert e.value.status == inr.INR_ERR_NONFINITE
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    inr.inr_fit_losses([m], out.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert out[2].item() == 1.0
+    # a NaN parameter, finite data
+    m2 = make_gpu_model(blk, 1, precision=prec, **NET)
+    p = np.empty(inr.inr_param_count(m2), np.float32)
+    inr.inr_get_params(m2, p)
+    p[-70] = np.nan                                        # a weight of the last layer
+    inr.inr_set_params(m2, p)
+    vt2 = gpu_volume(synth.g1_analytic(16).numpy())
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_fit(m2, whole_view(vt2), 1, 512, go, stream())
+    assert e.value.status == inr.INR_ERR_NONFINITE
+    inr.inr_destroy(m)
+    inr.inr_destroy(m2)
