@@ -167,3 +167,46 @@ def test_nonfinite_loss_and_parameters_are_reported(prec):
     assert e.value.status == inr.INR_ERR_NONFINITE
     inr.inr_destroy(m)
     inr.inr_destroy(m2)
+
+
+def test_single_model_decode_equals_group_decode(models):
+    """inr_decode (one model) is the group query with that model alone."""
+    gms, blocks = models["gms"], models["blocks"]
+    pts = synth.random_points(5000, (33, 33, 33))
+    pts = pts[(pts < 16).all(axis=1)]                       # block 0's points
+    pd = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    a = torch.empty(pts.shape[0], device="cuda")
+    b = torch.empty(pts.shape[0], device="cuda")
+    inr.inr_decode(gms[0], pd.data_ptr(), pts.shape[0], a.data_ptr(), 1, stream())
+    inr.inr_decode_group([gms[0]], pd.data_ptr(), pts.shape[0], b.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.isfinite(a).all()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_state_export_import_continues_bitwise(prec):
+    """inr_export_state / inr_import_state (block stealing): a fresh model that
+    imports another's state after 4 steps continues exactly like it."""
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[5]
+    vt = gpu_volume(synth.g1_analytic(32).numpy())
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = 0.0, 1.0, 64
+    a = make_gpu_model(blk, 3, reduction=1, precision=prec, **NET)
+    inr.inr_fit(a, whole_view(vt), 4, 1024, go, stream())
+    buf = torch.empty(inr.inr_state_bytes(a), dtype=torch.uint8, device="cuda")
+    inr.inr_export_state(a, buf.data_ptr(), stream())
+    b = make_gpu_model(blk, 3, reduction=1, precision=prec, **NET)
+    inr.inr_import_state(b, buf.data_ptr(), stream())
+    assert inr.inr_steps(b) == 4
+    inr.inr_fit(a, whole_view(vt), 3, 1024, go, stream())
+    inr.inr_fit(b, whole_view(vt), 3, 1024, go, stream())
+    pa = np.empty(inr.inr_param_count(a), np.float32)
+    pb = np.empty_like(pa)
+    inr.inr_get_params(a, pa)
+    inr.inr_get_params(b, pb)
+    assert np.array_equal(pa, pb)
+    other = make_gpu_model(sampler.decompose((32, 32, 32), (16, 16, 16))[6], 3, reduction=1, precision=prec, **NET)
+    with pytest.raises(inr.InrError):                       # another block's state is refused
+        inr.inr_import_state(other, buf.data_ptr(), stream())
+    for m in (a, b, other):
+        inr.inr_destroy(m)
