@@ -83,7 +83,10 @@ enum { INR_REDUCE_ATOMIC = 0,          /* fp32 atomics: fastest, run-to-run roun
  *   mlp_width W = 64 (this build), mlp_hidden_layers H in 1..8 (H hidden layers
  *   => H+1 weight matrices [R16]), out_dim D in {1, 3} (scalar or vector field,
  *   P:L156), mlp_bias in {0,1} [R15].
- *   L*F <= 64 and, for INR_PREC_FP16_MLP, a multiple of 16.
+ *   L*F <= 64 and, for INR_PREC_FP16_MLP, a multiple of 16; fitting in
+ *   INR_PREC_FP16_MLP also needs the tensor-memory weight-gradient accumulators
+ *   to fit, 64 + sum_k (in_k + 8) <= 512 columns (H <= 6 at L*F = 32, H <= 5 at
+ *   64), else inr_fit returns INR_ERR_UNSUPPORTED (decode has no such limit).
  *   seed selects the Philox4x32-10 streams for init (0), uniform samples (1),
  *   boundary samples (2) [R8, R14]. */
 typedef struct {

@@ -210,3 +210,19 @@ def test_state_export_import_continues_bitwise(prec):
         inr.inr_import_state(other, buf.data_ptr(), stream())
     for m in (a, b, other):
         inr.inr_destroy(m)
+
+
+def test_fp16_fit_too_deep_for_tmem_is_unsupported_but_decodes():
+    blk = sampler.decompose((16, 16, 16), (16, 16, 16))[0]
+    kw = dict(levels=16, features=2, log2_table_size=10, mlp_hidden_layers=8)   # 64 + 40 + 7 x 72 > 512
+    m = make_gpu_model(blk, 1, precision=1, **kw)
+    vt = gpu_volume(synth.g1_analytic(16).numpy())
+    go = inr.inr_fit_opts_default()
+    with pytest.raises(inr.InrError) as e:
+        inr.inr_fit(m, whole_view(vt), 1, 256, go, stream())
+    assert e.value.status == inr.INR_ERR_UNSUPPORTED
+    out = torch.full((16, 16, 16), float("nan"), device="cuda")
+    inr.inr_decode_grid(m, (16, 16, 16), out.data_ptr(), None, None, None, stream())
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    inr.inr_destroy(m)
