@@ -448,8 +448,8 @@ def run_ours(args):
     tot = dnr.allreduce_sum([float(ev_s), float(sk_s)])
     render = {"image": [W, H], "frame_ms": r_ms, "samples_evaluated": int(tot[0]), "samples_skipped": int(tot[1]),
               "evaluated_samples_per_s": tot[0] / (r_ms / 1e3), "waves_rank0": waves, "step": 0.5,
-              "path": "per-rank sample-streaming ray march (tensor-core queries, macro-cells), fragments gathered "
-                      "to rank 0 (NCCL) and depth-composited"}
+              "path": "per-rank sample-streaming ray march (tensor-core queries, macro-cells), fragments stored "
+                      "into rank 0's stack through NVLink peer memory, depth-composited there"}
     if img is not None:
         render["mean_alpha"] = float(img[:, 3].mean())
     del img

@@ -14,7 +14,8 @@ tests) is used only for the few reductions the method needs:
                     or the decode storing them into rank 0's volume through
                     NVLink peer memory (peer_volume / decode_to_rank)
 and for the consumers and training variants:
-  * render:         gather of sort-last fragments to rank 0
+  * render:         sort-last fragments stored into rank 0's stack through
+                    peer memory, then a barrier
   * fit_to_target:  per-round all-gather of unfinished blocks and send/recv
                     of stolen blocks' training state            (NEXT-4)
 
@@ -406,44 +407,61 @@ class DNR:
                stream=0, dst=0):
         """Sort-last DNR volume rendering (NEXT-3): this rank ray-marches
         its brick [lo, hi] (its blocks' span; neighbouring bricks share a face plane,
-        the half-open sample intervals split it) by direct queries, the fragments
-        are gathered to `dst` and depth-composited there.  cam / tf: inr_camera /
+        the half-open sample intervals split it) by direct queries; the fragment
+        kernels write straight into dst's fragment stack through NVLink peer memory
+        (no gather), and dst depth-composites them.  Collective at N > 1.  cam / tf: inr_camera /
         inr_transfer_fn.  Returns the RGBA image [H*W][4] on `dst`, None elsewhere."""
         span = float(tf.vmax - tf.vmin)
+        npix = cam.width * cam.height
+        dist_on = dist.is_available() and dist.is_initialized() and self.world > 1
+        if dist_on:
+            # the fragment stack lives on dst and every rank's fragment kernel writes its
+            # slice through NVLink peer memory (mapped once per image size)
+            key = (npix, dst)
+            if getattr(self, "_frag_key", None) != key:
+                self._frag_stack = self.peer_tensor((self.world, npix, 5), dst)
+                self._frag_key = key
+            stack, ptr = self._frag_stack
+            frag_ptr = ptr + 4 * 5 * npix * self.rank
+        else:
+            stack = torch.empty((1, npix, 5), dtype=torch.float32, device=torch.device("cuda", self.device))
+            frag_ptr = stack.data_ptr()
         r = self.inr.inr_renderer_create(self.models, cells, 1e-3 * span, stream)
         try:
-            npix = cam.width * cam.height
-            frag = torch.empty((npix, 5), dtype=torch.float32, device=torch.device("cuda", self.device))
             self.inr.inr_render(r, cam, tf, [float(v) for v in self.lo], [float(v) for v in self.hi], step,
-                                frag.data_ptr(), stop_alpha, int(use_macrocells), stream)
+                                frag_ptr, stop_alpha, int(use_macrocells), stream)
             self.last_render_stats = self.inr.inr_render_stats(r)
         finally:
             self.inr.inr_renderer_destroy(r)
         torch.cuda.current_stream().synchronize()
-        frags = gather_fragments(frag, dst)
-        if frags is None:
+        if dist_on:
+            dist.barrier()
+        if self.rank != dst:
             return None
-        img = torch.empty((npix, 4), dtype=torch.float32, device=frag.device)
-        self.inr.inr_composite(frags.data_ptr(), frags.shape[0], npix, background, img.data_ptr(), stream)
+        img = torch.empty((npix, 4), dtype=torch.float32, device=stack.device)
+        self.inr.inr_composite(stack.data_ptr(), stack.shape[0], npix, background, img.data_ptr(), stream)
         return img
 
-    def peer_volume(self, dst=0):
-        """Collective: rank `dst` allocates the global [z][y][x] volume and every
+    def peer_tensor(self, shape, dst=0):
+        """Collective: rank `dst` allocates an fp32 tensor of `shape` and every
         other rank maps it through NVLink peer memory (CUDA IPC, once).  Returns
-        (tensor on dst / None, device pointer of the volume on this rank)."""
+        (tensor on dst / None, device pointer of it on this rank)."""
         dev = torch.device("cuda", self.device)
-        gx, gy, gz = self.global_dims
-        full = torch.empty((gz, gy, gx) + ((self.D,) if self.D > 1 else ()), dtype=torch.float32,
-                           device=dev) if self.rank == dst else None
+        t = torch.empty(shape, dtype=torch.float32, device=dev) if self.rank == dst else None
         if not (dist.is_available() and dist.is_initialized() and self.world > 1):
-            return full, full.data_ptr()
+            return t, t.data_ptr()
         meta = [None] * self.world
-        dist.all_gather_object(meta, self.inr.inr_ipc_handle(full.data_ptr()) if self.rank == dst else None)
+        dist.all_gather_object(meta, self.inr.inr_ipc_handle(t.data_ptr()) if self.rank == dst else None)
         if self.rank == dst:
-            return full, full.data_ptr()
+            return t, t.data_ptr()
         ptr, base = self.inr.inr_ipc_open(meta[dst][0], meta[dst][1], self.device)
         self._peer_bases = getattr(self, "_peer_bases", []) + [base]
         return None, ptr
+
+    def peer_volume(self, dst=0):
+        """Collective: rank `dst`'s global [z][y][x] volume (peer_tensor)."""
+        gx, gy, gz = self.global_dims
+        return self.peer_tensor((gz, gy, gx) + ((self.D,) if self.D > 1 else ()), dst)
 
     def decode_to_rank(self, target, stream=0):
         """Decode every rank's blocks (1x) straight into the global volume of
