@@ -226,3 +226,27 @@ def test_fp16_fit_too_deep_for_tmem_is_unsupported_but_decodes():
     torch.cuda.synchronize()
     assert torch.isfinite(out).all()
     inr.inr_destroy(m)
+
+
+def test_block_psnrs_pool_to_the_global_psnr():
+    """DNR.block_psnrs: per-block SSE on each block's core nodes; the blocks tile
+    the volume, so their pooled MSE is the global one."""
+    from paper_2304_10516_b200 import dnr
+    vol = torch.from_numpy(synth.g1_analytic(40).numpy()).cuda()      # ragged: 40 = 16 + 16 + 8
+    d = dnr.DNR((40, 40, 40), (16, 16, 16), inr.make_config(precision=1, **NET))
+    lo, hi = d.value_range(vol, stream())
+    d.fit(vol, 30, 512, inr.inr_fit_opts_default(), stream(), report=False)
+    bp = d.block_psnrs(vol, stream())
+    out = torch.empty_like(vol)
+    sse = torch.zeros(1, dtype=torch.float64, device="cuda")
+    d.decode_grid_local(out, 1, vol, sse, stream())
+    torch.cuda.synchronize()
+    counts = {}
+    for b in d.block_ids:
+        o = dnr.block_origin(b, d.global_dims, d.n)
+        c = [min(16, 40 - o[k]) for k in range(3)]
+        counts[b] = c[0] * c[1] * c[2]
+    pooled = sum(10 ** (-bp[b] / 10) * counts[b] for b in bp) / 40 ** 3
+    assert abs(-10 * np.log10(pooled) - d.psnr(float(sse.item()), 40 ** 3)) < 1e-6
+    assert len(bp) == 27 and min(bp.values()) <= -10 * np.log10(pooled) + 1e-9
+    d.close()
