@@ -249,7 +249,7 @@ def run_ours(args):
     clk = clocks.stop(t_host0, t_host1)
     launches = inr.inr_kernel_launches() - launches0
     prof = {k: inr.inr_profile_read(k)
-            for k in ("step_begin", "sample", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "fit_fp32", "adam")}
+            for k in ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "fit_fp32", "adam")}
     inr.inr_profile_enable(0)
     ms_max = dnr.allreduce_max(ms)
     value = coords_per_step * world * args.steps / (ms_max / 1e3)

@@ -741,7 +741,6 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       if (tc) {
         // (the gradient is zeroed inside encode_fwd; step_begin only advances the step)
         { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, m0->net.nparams, s); }
-        { ProfScope p(PK_SAMPLE, s); launch_sample(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
         { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.targets, ws.dfeat, ws.Bs, s); }
@@ -759,7 +758,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     ~WsFree() { if (p) cudaFreeAsync(p, s); }
   } ws_free{ws_mem, st};
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = (tc ? 7 : 3) * nchunks;   // (graphs only without probing: fixed groups)
+  const int launches_per_step = (tc ? 6 : 3) * nchunks;   // (graphs only without probing: fixed groups)
   // CUDA graphs (launch-gap free): without probing, capture one step and replay it
   // per step; while profiling, capture the whole loop (with its event records)
   // once, so per-kernel timings come from the same graph execution.

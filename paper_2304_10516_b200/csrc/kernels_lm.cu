@@ -1,7 +1,8 @@
 // kernels_lm.cu — the CUDA-core stages of the level-major fp16 fit pipeline:
 //
-//   sample_kernel      x ~ Philox (uniform / boundary), trilinear target      (a2-a4)
-//   encode_fwd_kernel  per (level, sample): 8 corner gathers, blend -> fp16   (a5-a7)
+//   encode_fwd_kernel  per (level, sample): x ~ Philox (uniform / boundary),   (a2-a7)
+//                      8 corner gathers, blend -> fp16; level 0 also stores the
+//                      sample and its trilinear target(s)
 //   [mlp_fit_kernel, kernels_tc.cu: tensor-core MLP fwd, Eq. 2, bwd]          (a8-a10)
 //   encode_bwd_kernel  per (level, sample): scatter-add w_c * dfeat           (a11)
 //
@@ -22,30 +23,14 @@ constexpr int kLmThreads = 256;
 constexpr int kSmemAccFloats = 12288;   // levels with S_l * F <= this accumulate in smem (48 KB)
 constexpr int kBwdChunk = 2048;         // samples per CTA in the backward scatter
 
-// samples[i] = (x, y, z, t_0); vector fields also write targets[i] = (t_0, t_1, t_2, 0).
-template <int D>
-__global__ void __launch_bounds__(kLmThreads) sample_kernel(GroupArgs g, FitScalars fs, float4* __restrict__ samples,
-                                                             float4* __restrict__ targets, int Bs) {
-  const int m = blockIdx.y;
-  const ModelDev& md = g.md[m];
-  const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
-  const int i = blockIdx.x * kLmThreads + threadIdx.x;
-  if (i >= total) return;
-  const uint32_t step = (uint32_t)*md.step_cur;
-  float x[3], t[D];
-  draw_sample(md, i, fs.B_u, step, x);
-  sample_target<D>(md, x, t);
-  samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], t[0]);
-  if constexpr (D == 3) targets[(size_t)m * Bs + i] = make_float4(t[0], t[1], t[2], 0.f);
-}
-
 // Writes straight into the tensor-core MLP's h_0 tile images (canonical layout,
 // see tc_common.cuh): sample i -> tile i/128, row i%128, columns [l F, l F + F).
 // Padding samples (total <= i < Bs) write zeros; level 0 also writes the
 // constant-ones group (column LF).
 template <int F>
 __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, FitScalars fs,
-                                                                 const float4* __restrict__ samples,
+                                                                 float4* __restrict__ samples,
+                                                                 float4* __restrict__ targets,
                                                                  uint8_t* __restrict__ featimg, int Bs,
                                                                  FeatGeom geom) {
   const int m = blockIdx.z, l = blockIdx.y;
@@ -72,8 +57,22 @@ __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, Fit
 #pragma unroll
   for (int j = 0; j < F; ++j) f[j] = 0.f;
   if (i < total) {
-    const float4 s = __ldg(samples + (size_t)m * Bs + i);
-    const float x[3] = {s.x, s.y, s.z};
+    // the sample is drawn here (Philox, R8) for every level; level 0's CTAs also
+    // store it with its trilinear target(s) for the MLP and the scatter kernels
+    float x[3];
+    draw_sample(md, i, fs.B_u, (uint32_t)*md.step_cur, x);
+    if (l == 0) {
+      if (g.net.D == 1) {
+        float t[1];
+        sample_target<1>(md, x, t);
+        samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], t[0]);
+      } else {
+        float t[3];
+        sample_target<3>(md, x, t);
+        samples[(size_t)m * Bs + i] = make_float4(x[0], x[1], x[2], t[0]);
+        targets[(size_t)m * Bs + i] = make_float4(t[0], t[1], t[2], 0.f);
+      }
+    }
     encode_level<F>(md.params, g.net.lv[l], g.net.table_mask, x, f);
   }
   const int r = i & 127;
@@ -370,18 +369,12 @@ void launch_encode_query(const GroupArgs& g, const float4* qx, long long n, uint
   count_launch();
 }
 
-void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st) {
-  dim3 grid((fs.B_u + fs.B_b + kLmThreads - 1) / kLmThreads, nmodels);
-  if (g.net.D == 1) sample_kernel<1><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.targets, w.Bs);
-  else sample_kernel<3><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.targets, w.Bs);
-  count_launch();
-}
-
 void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w,
                        cudaStream_t st) {
   dim3 grid((w.Bs + kLmThreads - 1) / kLmThreads, g.net.L, nmodels);
   LM_DISPATCH_F(g.net.F,
-                encode_fwd_kernel<FF><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.featimg, w.Bs, w.geom));
+                encode_fwd_kernel<FF><<<grid, kLmThreads, 0, st>>>(g, fs, w.samples, w.targets, w.featimg, w.Bs,
+                                                                    w.geom));
   count_launch();
 }
 

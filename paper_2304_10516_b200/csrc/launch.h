@@ -138,7 +138,6 @@ size_t lm_workspace_bytes(const NetDesc& net, int nmodels, int Bs);
 LmWorkspace lm_workspace(void* base, const NetDesc& net, int nmodels, int Bs);
 void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStream_t st);
 
-void launch_sample(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 void launch_encode_bwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 bool tc_supported(const NetDesc& net);

@@ -38,12 +38,12 @@ def launches(path, out, cmd):
         a[1] += v
     ours = {k: v for k, v in agg.items() if k.startswith('inr::')}
     # one launch of each per fp16 fit step; prep_image also serves the decodes, so the
-    # share uses per-launch averages: avg(kernel) / sum of the seven averages
+    # share uses per-launch averages: avg(kernel) / sum of the step kernels' averages
     stepk = ('step_begin', 'sample_kernel', 'encode_fwd', 'prep_image', 'mlp_fit', 'encode_bwd', 'adam')
     step = sum(v[1] / v[0] for k, v in ours.items() if any(s in k for s in stepk))
     with open(out, 'w') as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised per launch)\n")
-        f.write(f"# command: {cmd}\n# libinr kernels only; share = avg launch / sum of the 7 fit-step kernels' "
+        f.write(f"# command: {cmd}\n# libinr kernels only; share = avg launch / sum of the fit-step kernels' "
                 "avg launches\n")
         f.write(f"# {'kernel':45s} launches   total_us     avg_us   share_of_fit_step\n")
         for k, (n, v) in ours.items():
