@@ -21,7 +21,7 @@ namespace inr {
 
 constexpr int kLmThreads = 256;
 constexpr int kSmemAccFloats = 12288;   // levels with S_l * F <= this accumulate in smem (48 KB)
-constexpr int kBwdChunk = 2048;         // samples per CTA in the backward scatter
+constexpr int kBwdChunk = 768;          // samples per CTA in the backward scatter (tuned: 512..2048 measured)
 
 // Writes straight into the tensor-core MLP's h_0 tile images (canonical layout,
 // see tc_common.cuh): sample i -> tile i/128, row i%128, columns [l F, l F + F).
