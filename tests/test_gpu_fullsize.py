@@ -94,3 +94,48 @@ def test_fullsize_decode_sampled(g2):
     assert normwise(q.cpu().numpy(), o_decode.decode_query(oms, pts)) <= 2e-3
     for m in gms:
         inr.inr_destroy(m)
+
+
+@pytest.mark.parametrize("prec", [1, 0])
+def test_fullsize_group_step_gradients(g2, prec):
+    """bench.py's exact fit launch: all 8 cfg2 blocks in one inr_fit_group call
+    (fp32 atomics).  Two sampled blocks (opposite corners of the block grid, so
+    different interior faces and Philox block counters) are put in the
+    branch-free regime (R27) and their one-step gradients checked entry by
+    entry against the oracle's full 81920-sample step; the other six blocks
+    train from their default init in the same launch."""
+    blocks = sampler.decompose(g2.shape[::-1], (BLOCK,) * 3)
+    cfg = oracle_config(**CFG2)
+    rng = np.random.default_rng(23)
+    picked = {0: None, 7: None}
+    for bi in picked:
+        picked[bi] = linear_regime(cfg, blocks[bi], g2, 13, B_U, B_B, rng)
+    # one shared range for the launch: a larger vmin only lowers every target,
+    # so sgn(y - t) = +1 holds for both sampled blocks
+    lo = max(v[1] for v in picked.values())
+    hi = lo + 1.0
+    opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=B_B)
+    ms = [make_gpu_model(b, 13, reduction=0, precision=prec, **CFG2) for b in blocks]
+    for bi, (p0, _, _, _) in picked.items():
+        inr.inr_set_params(ms[bi], p0)
+    vt = gpu_volume(g2)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = lo, hi, B_B
+    reps = inr.inr_fit_group(ms, [whole_view(vt)] * len(ms), 1, B_U, go, stream())
+    assert all(r.steps_taken == 1 for r in reps)
+    for bi, (p0, _, _, _) in picked.items():
+        om = InrModel(cfg, blocks[bi], 13, params=p0)
+        om.vmin, om.vmax = lo, hi
+        o_fit.train_step(om, g2, opts, B_U)
+        g = get_grads(ms[bi])
+        if prec == 0:
+            err = per_tensor_rel(cfg, g, om.g)
+            print(f"fp32 full-size group block {bi} per-tensor grad rel err", err)
+            assert err <= 1e-4
+        else:
+            r = componentwise_ratio(cfg, g, om.g, gradient_abs_bound(cfg, blocks[bi], 13, p0, g2, opts, B_U))
+            r /= 2.0 ** -11
+            print(f"fp16 full-size group block {bi} componentwise err / (u g_abs)", r)
+            assert r <= 2 * (cfg.mlp_hidden_layers + 2)
+    for m in ms:
+        inr.inr_destroy(m)
