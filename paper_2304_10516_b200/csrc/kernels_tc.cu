@@ -424,11 +424,13 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
       L.h_sbo[k] = (uint32_t)((in + L.ones) / 8) * 128;
       L.h[k] = take(kTileM * (in + L.ones) * 2, 1024);
     }
-  } else {       // forward only: two ping-pong buffers (layer k reads one, its epilogue writes the other)
-    const uint32_t hb[2] = {take(kTileM * 64 * 2, 1024), take(kTileM * 64 * 2, 1024)};
+  } else {       // forward only: one activation buffer.  Layer k's epilogue overwrites its own
+                 // input h_k with h_{k+1}: it runs after the MMA reading h_k has completed
+                 // (mbarrier), and the smaller footprint lets 5 CTAs share an SM
+    const uint32_t hb = take(kTileM * 64 * 2, 1024);
     for (int k = 0; k < net.H; ++k) {
       L.h_sbo[k] = (uint32_t)(net.in_dim[k] / 8) * 128;
-      L.h[k] = hb[k & 1];
+      L.h[k] = hb;
     }
   }
   L.feat_tile_bytes = kTileM * (net.LF + L.ones) * 2;
@@ -547,7 +549,7 @@ struct FwdArgs {
 };
 
 template <int F, int MODE, int D>
-__global__ void __launch_bounds__(kThreads, 4) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
+__global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
