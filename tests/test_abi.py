@@ -85,3 +85,43 @@ def test_argument_validation_without_device():
     assert L.inr_destroy(None) == inr.INR_OK
     assert L.cache_destroy(None) == inr.INR_OK
     assert L.cache_evict(None, None) == inr.INR_ERR_INVALID_ARG
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: importing the binding without libinr.so raises ImportError."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "try:\n    from paper_2304_10516_b200 import inr\nexcept ImportError as e:\n"
+            "    print('IMPORT_ERROR', e); sys.exit(0)\nsys.exit(3)\n") % ROOT
+    env = dict(os.environ, INR_LIB_PATH=str(tmp_path / "absent" / "libinr.so"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "no CPU fallback" in r.stdout, r.stdout + r.stderr
+
+
+def test_compute_without_a_device_is_a_cuda_error():
+    """Without a GPU a valid create fails with INR_ERR_CUDA (nothing runs on the host)."""
+    import ctypes
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    from paper_2304_10516_b200 import inr
+    h = ctypes.c_void_p()
+    cfg = inr.make_config(levels=4, log2_table_size=10)
+    blk = inr.make_block((0, 0, 0), (8, 8, 8), (9, 9, 9))
+    assert inr.lib.inr_create(ctypes.byref(cfg), ctypes.byref(blk), 0, ctypes.byref(h)) == inr.INR_ERR_CUDA
+
+
+def test_product_path_never_imports_the_oracle():
+    """oracle/ is test infrastructure: no module of the package or its CUDA sources
+    references it except in comments."""
+    import re
+    pkg = os.path.join(ROOT, "paper_2304_10516_b200")
+    for name in ("inr.py", "dnr.py", "__init__.py"):
+        src = open(os.path.join(pkg, name)).read()
+        assert not re.search(r"^\s*(from|import)\s+oracle\b|import_module\(['\"]oracle", src, re.M), name
+    for d, _, files in os.walk(os.path.join(pkg, "csrc")):
+        for f in files:
+            for line in open(os.path.join(d, f)):
+                code = line.split("//")[0]
+                assert "oracle" not in code, (f, line)
