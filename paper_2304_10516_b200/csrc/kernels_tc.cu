@@ -308,16 +308,33 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
     // ---- backward through the hidden layers
     for (int k = H - 1; k >= 0; --k) {
       const int in = net.in_dim[k];
+      // dz_k lives in dz / dz2 alternately, so dW_k may still read its tile while the
+      // epilogue writes dz_{k-1} into the other one
+      const uint32_t dzk = smem_u32(smem + (((H - 1 - k) & 1) ? lay.dz2 : lay.dz));
       if (t == 0) {
         fence_after();
-        // dW_k (+ db_k in column in_k): A = dz^T (MN-major), B = h_k (MN-major), K = 128 samples
-        gemm(tmem + lay.col_dw[k], smem_u32(smem + lay.dz), lay.dz_sbo, 128, 2 * lay.dz_sbo,
-             k == 0 ? h0 : smem_u32(smem + lay.h[k]), lay.h_sbo[k], 128, 2 * lay.h_sbo[k], kTileM / 16,
-             make_idesc(64, in + ones, 1, 1), !first);
-        // dh_k = dz_k W_k: A = dz (K-major, K = 64 outputs), B = W_k (MN-major, N = in_k)
-        gemm(tmem, smem_u32(smem + lay.dz), 128, lay.dz_sbo, 256, smem_u32(smem + lay.w[k]), lay.w_sbo[k], 128,
-             2 * lay.w_sbo[k], 64 / 16, make_idesc(128, in, 0, 1), false);
-        mma_commit(mbar);
+        auto dW = [&] {   // dW_k (+ db_k in column in_k): A = dz^T (MN-major), B = h_k (MN-major), K = 128 samples
+          gemm(tmem + lay.col_dw[k], dzk, lay.dz_sbo, 128, 2 * lay.dz_sbo,
+               k == 0 ? h0 : smem_u32(smem + lay.h[k]), lay.h_sbo[k], 128, 2 * lay.h_sbo[k], kTileM / 16,
+               make_idesc(64, in + ones, 1, 1), !first);
+        };
+        auto dH = [&] {   // dh_k = dz_k W_k: A = dz (K-major, K = 64 outputs), B = W_k (MN-major, N = in_k)
+          gemm(tmem, dzk, 128, lay.dz_sbo, 256, smem_u32(smem + lay.w[k]), lay.w_sbo[k], 128,
+               2 * lay.w_sbo[k], 64 / 16, make_idesc(128, in, 0, 1), false);
+        };
+        if (k > 0) {
+          // the epilogue waits for dh_k only; dW_k runs under it (the next commit, which
+          // every later wait follows, covers it: MMAs of one thread complete in order)
+          dH();
+          mma_commit(mbar);
+          dW();
+        } else {
+          // the last layer of the tile commits both: the next tile's TMA prefetch
+          // overwrites the h_0 buffer dW_0 reads
+          dW();
+          dH();
+          mma_commit(mbar);
+        }
       }
       mbar_wait(mbar, phase);
       phase ^= 1;
@@ -331,7 +348,8 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
 #pragma unroll
           for (int n = 0; n < 32; ++n) dh[n] = ((mask[k - 1] >> n) & 1u) ? dh[n] : 0.f;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dh + 8 * j);
+          for (int j = 0; j < 4; ++j)
+            st_row8(smem + (((H - k) & 1) ? lay.dz2 : lay.dz), lay.dz_sbo, r, hf * 4 + j, dh + 8 * j);
         } else if (valid) {
           // dfeat, unscaled, level-major (coalesced across the tile)
 #pragma unroll
@@ -437,6 +455,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   if (train) L.h0b = take(L.feat_tile_bytes, 1024);
   L.dz_sbo = 8 * 128;
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
+  if (train) L.dz2 = take(kTileM * 64 * 2, 1024);
   L.red = take((net.D * 65 + 1) * 8, 16);
   L.ypart = take(net.D * 2 * kTileM * 4, 16);
   L.mbar = take(8, 8);

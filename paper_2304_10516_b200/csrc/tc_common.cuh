@@ -22,6 +22,7 @@ struct Layout {
   uint32_t h[kMaxLayers];        // fp16 h_k tile [128 x (in_k + ones)] (k < H), h_0 = features
   uint32_t h_sbo[kMaxLayers];
   uint32_t dz, dz_sbo;           // fp16 dz tile [128 x 64]
+  uint32_t dz2;                  // second dz tile (backward layers alternate)
   uint32_t bias;                 // fp32 [H][64]
   uint32_t wout;                 // fp32 W_H[D][64], then b_H[D]
   uint32_t red;                  // dW_H[D][64], db_H[D] partials (fp32 or int64 fixed point)
