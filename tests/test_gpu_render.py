@@ -76,7 +76,7 @@ def test_render_brick_matches_oracle(scene):
     g = _gpu_frag(r, scene["tf"], lo, hi, 0.5, mc=0)
     o = _oracle_frag(scene, lo, hi, 0.5)
     assert o[:, 3].max() > 0.3 and (o[:, 3] > 0).mean() > 0.1     # a non-trivial image
-    _compare(g, o, 2e-4 if scene["prec"] == 0 else 1e-2)
+    _compare(g, o, 2.5e-6 if scene["prec"] == 0 else 2e-3)   # ~10x the measured 2.5e-7 / 1.9e-4
     ev, sk, waves = inr.inr_render_stats(r)
     assert ev > 0 and sk == 0 and waves >= 1
     inr.inr_renderer_destroy(r)

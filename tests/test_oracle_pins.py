@@ -217,6 +217,34 @@ def test_loss_linear_in_lambda():
     assert math.isclose(th, 0.7 * t0 + 0.3 * t1, rel_tol=1e-14)
 
 
+@pytest.mark.parametrize("lam", [0.0, 0.3, 0.8, 1.0])
+def test_loss_dy_matches_central_differences(lam):
+    """dL/dy of Eq. 2 against central differences of the pinned
+    total: L is piecewise linear in each y_i, so with every |y_i - t_i| > h the
+    difference quotient is exact up to rounding.  lam != 1/2 separates the
+    (1 - lam)/|U| uniform weight from the lam/|B| boundary weight (a swap of the
+    two, invisible at lam = 0.5, fails here); |U| != |B| separates the counts."""
+    rng = np.random.default_rng(31)
+    yu, tu = rng.random(9), rng.random(9)
+    yb, tb = rng.random(4), rng.random(4)
+    h = 1e-7
+    assert min(np.abs(yu - tu).min(), np.abs(yb - tb).min()) > 10 * h
+    _, _, _, dyu, dyb = loss.loss_and_grad(yu, tu, yb, tb, lam)
+
+    def total(a, b):
+        return loss.loss_and_grad(a, tu, b, tb, lam)[0]
+    for i in range(9):
+        e = np.zeros(9)
+        e[i] = h
+        fd = (total(yu + e, yb) - total(yu - e, yb)) / (2 * h)
+        assert math.isclose(dyu[i], fd, rel_tol=1e-6, abs_tol=1e-9)
+    for j in range(4):
+        e = np.zeros(4)
+        e[j] = h
+        fd = (total(yu, yb + e) - total(yu, yb - e)) / (2 * h)
+        assert math.isclose(dyb[j], fd, rel_tol=1e-6, abs_tol=1e-9)
+
+
 # ---------------------------------------------------------- P11 lr, P12 Adam
 def test_lr_schedule_examples():
     assert adam.lr_at(0) == 1e-2
@@ -276,6 +304,32 @@ def test_normalization_and_psnr():
     a = np.random.default_rng(10).random(1000)
     assert sampler.psnr(a, a) == 200.0
     assert math.isclose(sampler.psnr(a + 0.1, a), 20.0, rel_tol=1e-9)
+
+
+def test_probe_lattice_brute_force():
+    """The 32^3 cell-centred probe lattice:
+    enumerated by three plain loops, x fastest, every coordinate (j + 1/2)/32,
+    exact in fp32 (a dyadic rational)."""
+    xp = sampler.probe_lattice(32)
+    assert xp.shape == (32768, 3) and xp.dtype == np.float32
+    want = [((i + 0.5) / 32, (j + 0.5) / 32, (k + 0.5) / 32) for k in range(32) for j in range(32) for i in range(32)]
+    assert np.array_equal(xp, np.array(want, np.float32))
+    assert np.array_equal(sampler.probe_lattice(2), np.array([[.25, .25, .25], [.75, .25, .25], [.25, .75, .25],
+                                                              [.75, .75, .25], [.25, .25, .75], [.75, .25, .75],
+                                                              [.25, .75, .75], [.75, .75, .75]], np.float32))
+
+
+def test_sse_normalized_closed_forms():
+    """SSE in normalized units (R18): a uniform offset c (value units)
+    over n voxels gives n (c / (vmax - vmin))^2; a constant channel adds 0
+    (S:L70); per-channel spans divide per channel."""
+    from oracle import decode
+    ref = np.random.default_rng(11).random((5, 6, 7))
+    assert math.isclose(decode.sse_normalized(ref + 0.3, ref, 2.0, 4.0), 210 * 0.15 ** 2, rel_tol=1e-12)
+    assert decode.sse_normalized(ref, ref, 0.0, 1.0) == 0.0
+    r3 = np.zeros((4, 3))
+    p3 = r3 + [1.0, 2.0, 5.0]
+    assert math.isclose(decode.sse_normalized(p3, r3, [0, 0, 0], [2.0, 4.0, 0.0]), 4 * (0.25 + 0.25), rel_tol=1e-12)
 
 
 def test_value_range_permutation_invariant():
