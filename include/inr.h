@@ -406,16 +406,20 @@ INR_API inr_status inr_debug_encode(const inr_model* m, const float* x01, int64_
  * (dev q x 3 -> dev q x D), in the model's configured precision.  Asynchronous. */
 INR_API inr_status inr_debug_forward(const inr_model* m, const float* x01, int64_t q, float* y, cudaStream_t stream);
 /* Kernel timing for benchmarks: while enabled, every kernel the library
- * launches is bracketed by CUDA events recorded on its launching stream (and
- * the fit loop does not use CUDA graphs).  inr_profile_read synchronizes and
- * returns the summed device time (ms) and launch count of one kernel class:
- * "step_begin", "fit_fp32", "fit_tc", "adam", "decode_grid", "decode_query",
- * "probe", "range".  inr_profile_enable(1) also clears previous records. */
+ * launches is bracketed by CUDA events recorded on its launching stream.  A
+ * multi-step fit without probing is then captured as ONE CUDA graph of all its
+ * steps (event records included as graph nodes), instead of the one-step graph
+ * replayed per step when profiling is off; the kernels and their order are the
+ * same.  inr_profile_read synchronizes and returns the summed device time (ms)
+ * and launch count of one kernel class: "step_begin", "fit_fp32", "encode_fwd",
+ * "prep_image", "mlp_tc", "encode_bwd", "adam", "decode_grid", "decode_query",
+ * "probe", "range", "pathline".  inr_profile_enable(1) also clears previous
+ * records. */
 INR_API inr_status inr_profile_enable(int32_t on);
 INR_API inr_status inr_profile_read(const char* kernel, double* total_ms, int64_t* launches);
 /* Device time (ms) from the first recorded kernel start to the last recorded
- * kernel end since inr_profile_enable(1) (same stream), i.e. the span of the
- * timed work without host-side launch or graph-capture time. */
+ * kernel end since inr_profile_enable(1), i.e. the span of the timed work
+ * without host-side launch or graph-capture time. */
 INR_API inr_status inr_profile_span(double* span_ms);
 /* Number of kernels this library has launched since load (bench evidence). */
 INR_API int64_t inr_kernel_launches(void);

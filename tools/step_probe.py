@@ -1,0 +1,48 @@
+"""cfg2 fit-step time on the production path (no profiling: one-step CUDA graph
+replayed per step), CUDA events around K steps, median of R repeats; then one
+profiled K-step run for per-kernel-class device time.  Knobs via env
+(INR_SPAN_MB, INR_BWD_CHUNK, INR_ADAM_CTAS) are read by libinr at first use.
+
+  python tools/step_probe.py [K] [R]
+"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_2304_10516_b200 import dnr, inr
+
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+torch.cuda.set_stream(torch.cuda.Stream())
+st = torch.cuda.current_stream().cuda_stream
+cfg = inr.make_config(precision=1, seed=0x230410516, levels=16, features=2, log2_table_size=19, mlp_hidden_layers=3)
+d = dnr.DNR((256,) * 3, (128,) * 3, cfg)
+vol = synth.g2_energy(256, device="cuda").float().contiguous()
+d.value_range(vol, st)
+o = inr.inr_fit_opts_default()
+o.boundary_batch = 16384
+d.fit(vol, 10, 65536, o, st, report=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ts = []
+for r in range(R):
+    e0.record()
+    d.fit(vol, K, 65536, o, st, report=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) / K)
+ts.sort()
+inr.inr_profile_enable(1)
+d.fit(vol, K, 65536, o, st, report=False)
+torch.cuda.synchronize()
+span = inr.inr_profile_span()
+prof = {k: inr.inr_profile_read(k) for k in ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "adam")}
+inr.inr_profile_enable(0)
+rep = d.fit(vol, 1, 65536, o, st, report=True)
+env = {k: os.environ.get(k) for k in ("INR_SPAN_MB", "INR_BWD_CHUNK", "INR_ADAM_CTAS") if os.environ.get(k)}
+print(json.dumps({"env": env, "ms_per_step_median": ts[len(ts) // 2], "ms_per_step_all": ts,
+                  "coords_per_s": 8 * 81920 / (ts[len(ts) // 2] / 1e3),
+                  "profiled_span_ms_per_step": span / K,
+                  "per_step_ms": {k: v[0] / K for k, v in prof.items()},
+                  "launches_per_step": {k: v[1] / K for k, v in prof.items()}}))
+d.close()
