@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -542,9 +543,19 @@ extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
 }
 
 // Make sure device-resident parameters exist for a (possibly host-resident) model.
+// Staging is done once, under a lock, and completes before `staged` is set (the
+// stream is synchronized), so a later decode of the same snapshot on another
+// stream never reads a half-written staging buffer.
 static inr_status ensure_device_params(const inr_model* cm, cudaStream_t st) {
   inr_model* m = const_cast<inr_model*>(cm);
-  if (m->staged || (!m->host_resident && !m->h16)) return INR_OK;
+  if (!m->host_resident && !m->h16) return INR_OK;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (m->staged) return INR_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(INR_ERR_STATE, "a host-resident or fp16 cache snapshot is first decoded inside a stream capture");
   if (!m->params) CK(cudaMalloc((void**)&m->params, (size_t)m->P_pad * 4));
   if (m->h16) {   // fp16-stored snapshot: widen into the fp32 staging buffer
     const __half* src = m->h16;
@@ -560,6 +571,7 @@ static inr_status ensure_device_params(const inr_model* cm, cudaStream_t st) {
   } else {
     CK(cudaMemcpyAsync(m->params, m->host_params, (size_t)m->P_pad * 4, cudaMemcpyHostToDevice, st));
   }
+  CK(cudaStreamSynchronize(st));
   m->staged = true;
   return INR_OK;
 }

@@ -66,6 +66,18 @@ def local_node_box(block_ids, global_dims, n):
     return tuple(lo), tuple(hi)
 
 
+def is_block_box(block_ids, global_dims, n):
+    """True if the blocks fill an axis-aligned box of the block grid exactly (a
+    rank's local sub-volume, views, slab and render brick are that box)."""
+    if not block_ids:
+        return False
+    g = block_grid(global_dims, n)
+    coords = [(b % g[0], (b // g[0]) % g[1], b // (g[0] * g[1])) for b in block_ids]
+    lo = [min(c[d] for c in coords) for d in range(3)]
+    hi = [max(c[d] for c in coords) for d in range(3)]
+    return len(set(block_ids)) == (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1)
+
+
 def _dev():
     return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
 
@@ -200,6 +212,13 @@ class DNR:
         g = block_grid(self.global_dims, self.n)
         self.nblocks = g[0] * g[1] * g[2]
         self.block_ids = partition_blocks(self.nblocks, world, rank)
+        if not is_block_box(self.block_ids, self.global_dims, self.n):
+            # the local sub-volume, the decoded slab and the render brick are the
+            # bounding box of the rank's blocks: it must contain exactly those blocks
+            raise ValueError(f"rank {rank} of {world}: blocks {self.block_ids[:1]}..{self.block_ids[-1:]} of the "
+                             f"{g} block grid do not form an axis-aligned box; choose a world size whose block "
+                             f"ranges are whole rows / slabs (e.g. a divisor of the block count aligned to "
+                             f"{g[0]} x {g[1]})")
         self.rank, self.world = rank, world
         self.device = torch.cuda.current_device() if device is None else device
         self.lo, self.hi = local_node_box(self.block_ids, self.global_dims, self.n)
@@ -415,6 +434,9 @@ class DNR:
         npix = cam.width * cam.height
         dist_on = dist.is_available() and dist.is_initialized() and self.world > 1
         if dist_on:
+            # dst has finished compositing the previous frame (it synchronizes before
+            # returning) before any rank writes this frame's fragments into its stack
+            dist.barrier()
             # the fragment stack lives on dst and every rank's fragment kernel writes its
             # slice through NVLink peer memory (mapped once per image size)
             key = (npix, dst)
@@ -440,6 +462,8 @@ class DNR:
             return None
         img = torch.empty((npix, 4), dtype=torch.float32, device=stack.device)
         self.inr.inr_composite(stack.data_ptr(), stack.shape[0], npix, background, img.data_ptr(), stream)
+        if dist_on:
+            torch.cuda.current_stream().synchronize()   # the stack is free for the next frame's writes
         return img
 
     def peer_tensor(self, shape, dst=0):

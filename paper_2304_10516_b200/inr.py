@@ -278,6 +278,8 @@ def inr_fit(m, view, steps, batch, opts, stream=0, report=True):
 
 
 def inr_fit_group(models, views, steps, batch, opts, stream=0, report=True):
+    if len(views) != len(models):
+        raise ValueError(f"{len(models)} models but {len(views)} views")
     pp, keep = _ptrs(models)
     va = (inr_view * len(views))(*views)
     reps = (inr_fit_report * len(models))() if report else None
@@ -301,6 +303,9 @@ def inr_decode_group(models, xyz_ptr, q, out_ptr, strict=0, stream=0):
 
 
 def inr_decode_grid(m, res, out_ptr, out_stride=None, ref_ptr=None, sse_ptr=None, stream=0, count=None):
+    for name, t in (("res", res), ("out_stride", out_stride), ("count", count)):
+        if t is not None and len(t) != 3:
+            raise ValueError(f"{name} must have 3 entries (x, y, z), got {len(t)}")
     r = (_I32 * 3)(*res)
     s = (_I64 * 3)(*out_stride) if out_stride is not None else None
     if count is None:

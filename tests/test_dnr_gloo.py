@@ -29,6 +29,20 @@ def test_block_geometry_and_local_box():
     assert dnr.local_node_box(ids, g, (128,) * 3) == ((0, 0, 256), (255, 255, 511))
 
 
+def test_block_box_check():
+    """A rank's blocks must form an axis-aligned box (its sub-volume, slab and
+    render brick are their bounding box): cfg3's 64 blocks split in 1/2/4/8
+    and cfg2's weak-scaling slabs do; 64 blocks on 3 ranks do not."""
+    g3, n = (512, 512, 512), (128,) * 3
+    for w in (1, 2, 4, 8, 16):
+        assert all(dnr.is_block_box(dnr.partition_blocks(64, w, r), g3, n) for r in range(w)), w
+    assert not all(dnr.is_block_box(dnr.partition_blocks(64, 3, r), g3, n) for r in range(3))
+    assert not dnr.is_block_box([0, 1, 2, 3, 4], g3, n)          # a row and a stray block
+    assert dnr.is_block_box([5], g3, n) and not dnr.is_block_box([], g3, n)
+    g2 = (256, 256, 256 * 4)
+    assert all(dnr.is_block_box(dnr.partition_blocks(32, 4, r), g2, n) for r in range(4))
+
+
 def test_psnr_from_sse():
     assert dnr.psnr_from_sse(0.0, 10) == 200.0
     assert abs(dnr.psnr_from_sse(0.01 * 10, 10) - 20.0) < 1e-12
