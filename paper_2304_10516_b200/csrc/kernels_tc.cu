@@ -463,6 +463,8 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   L.mbar_feat[0] = take(8, 8);
   L.mbar_feat[1] = take(8, 8);
   L.tslot = take(4, 4);
+  if (!train) L.stage = take(kStageFloats * 4, 16);
+  if (!train) L.stbox = take(kMaxLevels * 8 * 4, 16);
   // TMEM: [0, 64) layer accumulator; then dW_k (M = 64 rows, in_k + ones columns)
   // (8-column granularity; the last region is padded so 16-column loads stay inside)
   uint32_t col = 64;
@@ -484,6 +486,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   if (need > 232448u) return false;
   // actual residency is then limited by both shared memory and TMEM
   L.ctas_per_sm = std::min<int>(L.ctas_per_sm, (int)(232448u / L.bytes));
+  if (!train) L.ctas_per_sm = std::min(L.ctas_per_sm, 4);   // forward_tc_kernel: 256 threads x <= 64 registers
   return L.ctas_per_sm >= 1;
 }
 
@@ -565,16 +568,78 @@ struct FwdArgs {
   const uint8_t* wimg;   // prepared weight images, one per model slot (prep_image_kernel)
   const uint8_t* featimg;   // MODE 3: h_0 tile images of tiles [tile0, tile1)
   long long tile0, tile1;
+  int nst;                            // MODE 1: levels [0, nst) are staged per brick in shared memory
+  int st_off[kMaxLevels + 1];         //   float offset of level l's vertex box in the stage area
+  int na;                             // MODE 1: levels [na, L) are vertex-aligned (one entry per point, R19)
 };
 
+// MODE 1 brick staging (grid decode): the levels coarser than the
+// lattice (N_l < R) have fractional weights at most lattice points, and the
+// 128 points of an 8 x 4 x 4 brick touch only a small box of their vertices
+// (cfg2, R = 128: 27-45 vertices per level instead of 8 corner reads per point).
+// The box is computed from the brick's first and last lattice point per axis
+// with the same pinned index arithmetic as level_cell (R4, R20).
+__device__ __forceinline__ int cell_of(float x, uint32_t res) {
+  const float p = __fmul_rn(fminf(fmaxf(x, 0.f), 1.f), (float)res);
+  return min((int)floorf(p), (int)res - 1);
+}
+
+__device__ __forceinline__ uint32_t vertex_index(uint32_t vx, uint32_t vy, uint32_t vz, const LevelInfo& lv,
+                                                 uint32_t mask) {
+  if (lv.dense) {
+    const uint32_t s = lv.res + 1;
+    return vx + s * (vy + s * vz);
+  }
+  return (vx ^ (vy * kPrimeY) ^ (vz * kPrimeZ)) & mask;
+}
+
+// feat = sum_c w_c theta[idx_c] from the staged box (lo, n): the same weights
+// (corner_weight) and the same corner-ordered fma chain as encode_level, so the
+// result is bitwise the global-memory encode (grid == query decode stays exact).
+template <int F>
+__device__ __forceinline__ void blend_staged(const float* __restrict__ box, const int lo[3], const int n[3],
+                                             uint32_t res, const float x[3], float feat[F]) {
+  Cell cell = level_cell(x, res);
+#pragma unroll
+  for (int f = 0; f < F; ++f) feat[f] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int vx = (int)cell.i[0] + (c & 1) - lo[0];
+    const int vy = (int)cell.i[1] + ((c >> 1) & 1) - lo[1];
+    const int vz = (int)cell.i[2] + ((c >> 2) & 1) - lo[2];
+    const float* e = box + (vx + n[0] * (vy + n[1] * vz)) * F;
+    const float w = corner_weight(cell, c);
+#pragma unroll
+    for (int f = 0; f < F; ++f) feat[f] = fmaf(w, e[f], feat[f]);
+  }
+}
+
+// fp16 feature columns [c, c + F) of this thread's h_0 row (canonical layout)
+template <int F>
+__device__ __forceinline__ void put_feat(uint8_t* row, int c, const float fl[F]) {
+  if constexpr (F == 1) {
+    *reinterpret_cast<__half*>(row + (c >> 3) * 128 + (c & 7) * 2) = __float2half_rn(fl[0]);
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < F; jj += 2)
+      *reinterpret_cast<__half2*>(row + ((c + jj) >> 3) * 128 + ((c + jj) & 7) * 2) = __floats2half2_rn(fl[jj], fl[jj + 1]);
+  }
+}
+
+// 256 threads per 128-point tile: thread t owns row r = t % 128 (TMEM lane r) and
+// half hf = t / 128, which encodes every other level (l % 2 == hf) and, in the
+// epilogues, columns [32 hf, 32 hf + 32): half the serial work per thread of a
+// one-thread-per-row tile, at ~64 registers, so 4 CTAs (32 warps) share an SM.
 template <int F, int MODE, int D>
-__global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
+__global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g, FwdArgs a, Layout lay) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const NetDesc& net = g.net;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int r = t & (kTileM - 1), hf = t >> 7, cb = hf * 32;
   const int H = net.H;
-  float* bias = reinterpret_cast<float*>(smem + lay.bias);
+  const float* bias = reinterpret_cast<const float*>(smem + lay.bias);
   float* wout = reinterpret_cast<float*>(smem + lay.wout);
+  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [D][2][128] output-layer half sums
   const uint32_t mbar = smem_u32(smem + lay.mbar);
   const uint32_t mbar_img = smem_u32(smem + lay.mbar_img);
   const uint32_t mbar_feat = smem_u32(smem + lay.mbar_feat[0]);
@@ -594,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   uint32_t phase = 0, img_phase = 0, feat_phase = 0;
   int cur = -1;  // model whose weight image is in smem
   // tiles are visited grid-stride: the CTAs in flight work on consecutive tiles
@@ -602,7 +667,9 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
   // CTA reloads the weight image only when its next tile belongs to another block
   long long t0 = blockIdx.x, t1;
   if constexpr (MODE == 0) t1 = (a.q + kTileM - 1) / kTileM;
-  else if constexpr (MODE == 1) t1 = ((long long)a.cnt[0] * a.cnt[1] * a.cnt[2] + kTileM - 1) / kTileM;
+  else if constexpr (MODE == 1)
+    t1 = (long long)((a.cnt[0] + kBrickX - 1) / kBrickX) * ((a.cnt[1] + kBrickY - 1) / kBrickY) *
+         ((a.cnt[2] + kBrickZ - 1) / kBrickZ);
   else { t0 += a.tile0; t1 = min(a.tile1, (long long)*a.ntiles_dev); }
   const long long tstep = gridDim.x;
   for (long long tile = t0; tile < t1; tile += tstep) {
@@ -619,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
     }
     const ModelDev& md = g.md[slot];
     const float* P = md.params;
-    const long long j = tile * kTileM + t;
+    const long long j = tile * kTileM + r;
     bool valid;
     float x[3] = {0.f, 0.f, 0.f};
     long long dst = 0;
@@ -627,20 +694,40 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
       valid = j < a.q;
       if (valid) { x[0] = __ldg(a.x01 + 3 * j); x[1] = __ldg(a.x01 + 3 * j + 1); x[2] = __ldg(a.x01 + 3 * j + 2); }
     } else if constexpr (MODE == 1) {
-      valid = j < (long long)a.cnt[0] * a.cnt[1] * a.cnt[2];
-      if (valid) {
-        const int jx = (int)(j % a.cnt[0]);
-        const long long r = j / a.cnt[0];
-        const int jy = (int)(r % a.cnt[1]), jz = (int)(r / a.cnt[1]);
-        x[0] = __fdiv_rn((float)jx, (float)a.res[0]);
-        x[1] = __fdiv_rn((float)jy, (float)a.res[1]);
-        x[2] = __fdiv_rn((float)jz, (float)a.res[2]);
-        if (md.mesh[0]) {   // rectilinear (R36): the block's nodes
-          const int jj[3] = {jx, jy, jz};
+      // brick (bx, by, bz) of 8 x 4 x 4 lattice points; points past cnt are computed
+      // at the clamped (last) lattice point and not stored
+      // (32-bit: a grid whose output fits in device memory has < 2^31 bricks)
+      const unsigned nbx = (a.cnt[0] + kBrickX - 1) / kBrickX, nby = (a.cnt[1] + kBrickY - 1) / kBrickY;
+      const unsigned tu = (unsigned)tile, rr = tu / nbx;
+      const int bx = (int)(tu - rr * nbx), by = (int)(rr % nby), bz = (int)(rr / nby);
+      const int jx = bx * kBrickX + (r & 7), jy = by * kBrickY + ((r >> 3) & 3), jz = bz * kBrickZ + (r >> 5);
+      valid = jx < a.cnt[0] && jy < a.cnt[1] && jz < a.cnt[2];
+      const int jj[3] = {min(jx, a.cnt[0] - 1), min(jy, a.cnt[1] - 1), min(jz, a.cnt[2] - 1)};
 #pragma unroll
-          for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
+      for (int d = 0; d < 3; ++d) x[d] = __fdiv_rn((float)jj[d], (float)a.res[d]);
+      if (md.mesh[0]) {   // rectilinear (R36): the block's nodes (no staging: nst = 0)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
+      }
+      dst = jx * a.os[0] + jy * a.os[1] + jz * a.os[2];
+      if (a.nst > 0 && t < 32) {
+        // the brick's vertex box per staged level (lane l: level l): lo / n per axis from
+        // the brick's first and last lattice point, with level_cell's pinned arithmetic
+        int* box = reinterpret_cast<int*>(smem + lay.stbox);
+        if (t < a.nst) {
+          const int b0[3] = {bx * kBrickX, by * kBrickY, bz * kBrickZ};
+          const int b1[3] = {min(b0[0] + kBrickX, a.cnt[0]) - 1, min(b0[1] + kBrickY, a.cnt[1]) - 1,
+                             min(b0[2] + kBrickZ, a.cnt[2]) - 1};
+          const uint32_t res = net.lv[t].res;
+          int lo[3], n[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            lo[d] = cell_of(__fdiv_rn((float)b0[d], (float)a.res[d]), res);
+            n[d] = cell_of(__fdiv_rn((float)b1[d], (float)a.res[d]), res) + 2 - lo[d];
+          }
+          *reinterpret_cast<int4*>(box + 8 * t) = make_int4(lo[0], lo[1], lo[2], n[0]);
+          *reinterpret_cast<int4*>(box + 8 * t + 4) = make_int4(n[1], n[2], n[0] * n[1] * n[2], 0);
         }
-        dst = jx * a.os[0] + jy * a.os[1] + jz * a.os[2];
       }
     } else {
       const int qi = a.perm[j];
@@ -656,30 +743,88 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
       mbar_wait(mbar_feat, feat_phase);
       feat_phase ^= 1;
     } else {
-      // features straight into this thread's row of the h_0 tile (no staging array)
-      uint8_t* row = smem + lay.h[0] + (t & 7) * 16 + (t >> 3) * lay.h_sbo[0];
-#pragma unroll 4
-      for (int l = 0; l < net.L; ++l) {   // unrolled: several levels' gathers in flight
-        float fl[F];
-        if (MODE == 0) encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
-        else encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
-        const int c = l * F;
-        if constexpr (F == 1) {
-          *reinterpret_cast<__half*>(row + (c >> 3) * 128 + (c & 7) * 2) = __float2half_rn(fl[0]);
-        } else {
+      // features straight into row r of the h_0 tile; this thread: levels l = hf, hf + 2, ...
+      uint8_t* row = smem + lay.h[0] + (r & 7) * 16 + (r >> 3) * lay.h_sbo[0];
+      if constexpr (MODE == 0) {
+#pragma unroll 2
+        for (int l = hf; l < net.L; l += 2) {
+          float fl[F];
+          encode_level<F>(P, net.lv[l], net.table_mask, x, fl);
+          put_feat<F>(row, l * F, fl);
+        }
+      } else {
+        // this half's vertex-aligned fine levels (R19: one entry each) are gathered in
+        // batches whose loads are all in flight before any is used; the first batch
+        // flies while this half's staged coarse levels blend from shared memory
+        constexpr int NB = F == 1 ? 8 : F == 2 ? 6 : 16 / F;   // batch: <= 16 fp32 registers of gathered entries
+        FVec<F> e[NB];
+        const int lf0 = a.na + ((a.na & 1) != hf);   // this half's first aligned level
+        auto issue = [&](int l0) {
 #pragma unroll
-          for (int jj = 0; jj < F; jj += 2)
-            *reinterpret_cast<__half2*>(row + ((c + jj) >> 3) * 128 + ((c + jj) & 7) * 2) =
-                __floats2half2_rn(fl[jj], fl[jj + 1]);
+          for (int u = 0; u < NB; ++u)
+            if (l0 + 2 * u < net.L) {
+              const LevelInfo& lv = net.lv[l0 + 2 * u];
+              const Cell cell = level_cell(x, lv.res);
+              e[u] = load_entry<F>(P + lv.offset + (size_t)corner_index(cell, 0, lv, net.table_mask) * F);
+            }
+        };
+        auto consume = [&](int l0) {
+#pragma unroll
+          for (int u = 0; u < NB; ++u)
+            if (l0 + 2 * u < net.L) {
+              float fl[F];
+#pragma unroll
+              for (int f = 0; f < F; ++f) fl[f] = fmaf(1.f, e[u].v[f], 0.f);   // == the 8-corner sum (R19)
+              put_feat<F>(row, (l0 + 2 * u) * F, fl);
+            }
+        };
+        issue(lf0);
+        if (a.nst > 0) {
+          // stage the staged levels' vertex boxes: one entry per thread over the
+          // concatenated boxes (every load in flight at once, with the fine gathers above)
+          __syncthreads();   // the box table
+          const int* box = reinterpret_cast<const int*>(smem + lay.stbox);
+          float* stage = reinterpret_cast<float*>(smem + lay.stage);
+          int l = 0, base = 0;
+          for (int v = t;; v += kFwdThreads) {
+            while (l < a.nst && v >= base + box[8 * l + 6]) base += box[8 * l + 6], ++l;
+            if (l >= a.nst) break;
+            const int4 b4 = *reinterpret_cast<const int4*>(box + 8 * l);
+            const int n1 = box[8 * l + 4];
+            const int w = v - base;
+            const int vx = w % b4.w, vy = (w / b4.w) % n1, vz = w / (b4.w * n1);
+            const LevelInfo& lv = net.lv[l];
+            const uint32_t idx = vertex_index(b4.x + vx, b4.y + vy, b4.z + vz, lv, net.table_mask);
+            const FVec<F> ev = load_entry<F>(P + lv.offset + (size_t)idx * F);
+#pragma unroll
+            for (int f = 0; f < F; ++f) stage[a.st_off[l] + w * F + f] = ev.v[f];
+          }
+          __syncthreads();   // the staged entries
+        }
+        for (int l = hf; l < a.na; l += 2) {
+          float fl[F];
+          if (l < a.nst) {
+            const int* box = reinterpret_cast<const int*>(smem + lay.stbox) + 8 * l;
+            const int4 b4 = *reinterpret_cast<const int4*>(box);
+            const int4 b5 = *reinterpret_cast<const int4*>(box + 4);
+            const int lo[3] = {b4.x, b4.y, b4.z}, n[3] = {b4.w, b5.x, b5.y};
+            blend_staged<F>(reinterpret_cast<const float*>(smem + lay.stage) + a.st_off[l], lo, n, net.lv[l].res, x,
+                            fl);
+          } else {
+            encode_level_infer<F>(P, net.lv[l], net.table_mask, x, fl);
+          }
+          put_feat<F>(row, l * F, fl);
+        }
+        consume(lf0);
+        for (int l0 = lf0 + 2 * NB; l0 < net.L; l0 += 2 * NB) {
+          issue(l0);
+          consume(l0);
         }
       }
     }
     fence_async_smem();
     fence_before();
     __syncthreads();
-    float y[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) y[c] = wout[D * 64 + c];
     for (int k = 0; k < H; ++k) {
       if (t == 0) {
         fence_after();
@@ -690,57 +835,78 @@ __global__ void __launch_bounds__(kThreads, 5) forward_tc_kernel(GroupArgs g, Fw
       mbar_wait(mbar, phase);
       phase ^= 1;
       fence_after();
-      float z[64];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_base + c * 16, z + c * 16);
+      float z[32];
+      tmem_ld16(tmem + lane_base + cb, z);
+      tmem_ld16(tmem + lane_base + cb + 16, z + 16);
       tmem_wait_ld();
 #pragma unroll
-      for (int n = 0; n < 64; n += 4) {
-        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + n);
-        z[n] = fmaxf(z[n] + b4.x, 0.f);
-        z[n + 1] = fmaxf(z[n + 1] + b4.y, 0.f);
-        z[n + 2] = fmaxf(z[n + 2] + b4.z, 0.f);
-        z[n + 3] = fmaxf(z[n + 3] + b4.w, 0.f);
+      for (int n = 0; n < 32; n += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + cb + n);
+        z[n] += b4.x;
+        z[n + 1] += b4.y;
+        z[n + 2] += b4.z;
+        z[n + 3] += b4.w;
       }
       if (k + 1 < H) {
+        // ReLU on packed fp16 pairs: max(round(z + b), 0) == round(max(z + b, 0))
+        uint8_t* tile = smem + lay.h[k + 1] + (r & 7) * 16 + (r >> 3) * lay.h_sbo[k + 1] + hf * 4 * 128;
+        const __half2 zero2 = __float2half2_rn(0.f);
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], t, jj, z + 8 * jj);
-      } else {   // the 64 -> D output layer, fp32 on CUDA cores
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          __half2 h0 = __hmax2(__floats2half2_rn(z[8 * q], z[8 * q + 1]), zero2);
+          __half2 h1 = __hmax2(__floats2half2_rn(z[8 * q + 2], z[8 * q + 3]), zero2);
+          __half2 h2 = __hmax2(__floats2half2_rn(z[8 * q + 4], z[8 * q + 5]), zero2);
+          __half2 h3 = __hmax2(__floats2half2_rn(z[8 * q + 6], z[8 * q + 7]), zero2);
+          u.x = *reinterpret_cast<uint32_t*>(&h0);
+          u.y = *reinterpret_cast<uint32_t*>(&h1);
+          u.z = *reinterpret_cast<uint32_t*>(&h2);
+          u.w = *reinterpret_cast<uint32_t*>(&h3);
+          *reinterpret_cast<uint4*>(tile + q * 128) = u;
+        }
+      } else {   // the 64 -> D output layer, fp32 on CUDA cores: this half's 32 columns
 #pragma unroll
-        for (int n = 0; n < 64; ++n) {
+        for (int c = 0; c < D; ++c) {
+          float yp = 0.f;
 #pragma unroll
-          for (int c = 0; c < D; ++c) y[c] = fmaf(wout[c * 64 + n], z[n], y[c]);
+          for (int n = 0; n < 32; ++n) yp = fmaf(wout[c * 64 + cb + n], fmaxf(z[n], 0.f), yp);
+          ypart[(2 * c + hf) * kTileM + r] = yp;
         }
       }
       fence_async_smem();
       fence_before();
       __syncthreads();
     }
-    if constexpr (MODE == 0) {
-      if (valid) {
+    if (hf == 0) {
+      float y[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) a.y[j * D + c] = y[c];
-      }
-    } else {
-      double e = 0.0;
-      if (valid) {
-        if constexpr (MODE == 3) dst *= D;   // query outputs: q x D, channels interleaved
+      for (int c = 0; c < D; ++c) y[c] = wout[D * 64 + c] + ypart[(2 * c) * kTileM + r] + ypart[(2 * c + 1) * kTileM + r];
+      if constexpr (MODE == 0) {
+        if (valid) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-          const float v = fmaf(y[c], md.vrange[c], md.vmin[c]);
-          a.out[dst + c] = v;
-          if (MODE == 1 && a.ref) {
-            // a constant channel (vrange 0) is 0 in normalized units on both sides
-            const double dd =
-                md.vrange[c] > 0.f ? ((double)v - (double)__ldg(a.ref + dst + c)) / (double)md.vrange[c] : 0.0;
-            e += dd * dd;
+          for (int c = 0; c < D; ++c) a.y[j * D + c] = y[c];
+        }
+      } else {
+        double e = 0.0;
+        if (valid) {
+          if constexpr (MODE == 3) dst *= D;   // query outputs: q x D, channels interleaved
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const float v = fmaf(y[c], md.vrange[c], md.vmin[c]);
+            a.out[dst + c] = v;
+            if (MODE == 1 && a.ref) {
+              // a constant channel (vrange 0) is 0 in normalized units on both sides
+              const double dd =
+                  md.vrange[c] > 0.f ? ((double)v - (double)__ldg(a.ref + dst + c)) / (double)md.vrange[c] : 0.0;
+              e += dd * dd;
+            }
           }
         }
-      }
-      if (MODE == 1 && a.sse) {
+        if (MODE == 1 && a.sse) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (lane == 0 && e != 0.0) atomicAdd(a.sse, e);
+          for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+          if (lane == 0 && e != 0.0) atomicAdd(a.sse, e);
+        }
       }
     }
   }
@@ -762,7 +928,7 @@ static void launch_forward(const GroupArgs& g, const FwdArgs& a0, long long ntil
 #define CASE_FD(FF, DD)                                                                                             \
   case FF * 10 + DD:                                                                                                \
     cudaFuncSetAttribute(forward_tc_kernel<FF, MODE, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);   \
-    forward_tc_kernel<FF, MODE, DD><<<grid, kThreads, L.bytes, st>>>(g, a, L);                                     \
+    forward_tc_kernel<FF, MODE, DD><<<grid, kFwdThreads, L.bytes, st>>>(g, a, L);                                     \
     break;
     CASE_FD(1, 1) CASE_FD(2, 1) CASE_FD(4, 1) CASE_FD(8, 1) CASE_FD(1, 3) CASE_FD(2, 3) CASE_FD(4, 3) CASE_FD(8, 3)
 #undef CASE_FD
@@ -801,8 +967,38 @@ void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res
   a.out = out;
   a.ref = ref;
   a.sse = sse;
-  long long n = (long long)cnt[0] * cnt[1] * cnt[2];
-  launch_forward<1>(*single_group(net, md), a, (n + kTileM - 1) / kTileM, st);
+  // staged levels: the coarse levels (N_l < R on every axis) whose worst-case vertex
+  // box per brick, (ceil((B_d - 1) N_l / R_d) + 2) per axis, fits the stage area
+  const int B[3] = {kBrickX, kBrickY, kBrickZ};
+  int off = 0;
+  a.nst = 0;
+  a.st_off[0] = 0;
+  for (int l = 0; l < net.L && !md.mesh[0]; ++l) {
+    const long long N = net.lv[l].res;
+    long long cap = 1;
+    bool coarse = true;
+    for (int d = 0; d < 3; ++d) {
+      coarse &= N < res[d];
+      cap *= ((long long)(B[d] - 1) * N + res[d] - 1) / res[d] + 2;
+    }
+    if (!coarse || off + cap * net.F > kStageFloats) break;
+    off += (int)cap * net.F;
+    a.nst = l + 1;
+    a.st_off[l + 1] = off;
+  }
+  // vertex-aligned levels: x_j = j / R_d is exact (R_d a power of two) and N_l a
+  // multiple of R_d, so x_j N_l is an integer vertex for every lattice point (R19)
+  a.na = net.L;
+  for (int l = net.L - 1; l >= a.nst && !md.mesh[0]; --l) {
+    bool al = true;
+    for (int d = 0; d < 3; ++d)
+      al &= (res[d] & (res[d] - 1)) == 0 && net.lv[l].res % (uint32_t)res[d] == 0;
+    if (!al) break;
+    a.na = l;
+  }
+  const long long nb = (long long)((cnt[0] + kBrickX - 1) / kBrickX) * ((cnt[1] + kBrickY - 1) / kBrickY) *
+                       ((cnt[2] + kBrickZ - 1) / kBrickZ);
+  launch_forward<1>(*single_group(net, md), a, nb, st);
 }
 
 // Queries: per chunk of <= 2^15 bucketed tiles, x per query (query_prep_kernel),

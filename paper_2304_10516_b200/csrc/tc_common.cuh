@@ -15,6 +15,10 @@ namespace tc {
 
 constexpr int kThreads = 128;
 constexpr int kTileM = 128;
+// grid decode tiles are 8 x 4 x 4 bricks of lattice points (thread t <-> (t & 7, (t >> 3) & 3, t >> 5))
+constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4;
+constexpr int kStageFloats = 640;    // smem floats for the staged coarse-level vertices of one brick
+constexpr int kFwdThreads = 256;     // forward-only kernel: thread t <-> row t % 128, column / level half t / 128
 
 struct Layout {
   uint32_t w[kMaxLayers];        // fp16 W_k tile [64 x in_k] (k < H)
@@ -34,10 +38,12 @@ struct Layout {
   uint32_t img_bytes;            // [0, img_bytes): weight tiles + biases + output layer (the weight image)
   uint32_t feat_tile_bytes;      // one 128-sample h_0 tile image
   uint32_t tslot;                // 4 B: TMEM base address
+  uint32_t stage;                // forward only: per-brick staging of coarse-level vertices (kStageFloats fp32)
   uint32_t bytes;                // dynamic smem requested
   uint32_t col_dw[kMaxLayers];   // TMEM column of the dW_k accumulator
   uint32_t ncols;                // TMEM columns allocated (power of 2)
   int ones;                      // 8 if biases (ones group appended), else 0
+  uint32_t stbox;                // forward only: per staged level int[8] = lo[3], n[3] of the brick's vertex box
   int ctas_per_sm;
 };
 
