@@ -200,8 +200,10 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
                fbar[b ^ 1]);
     }
     mbar_wait(fbar[b], (uint32_t)(it >> 1) & 1u);
-    // ---- forward through the hidden layers (this thread: columns [cb, cb + 32))
-    uint32_t mask[kMaxLayers];
+    // ---- forward through the hidden layers (this thread: columns [cb, cb + 32)).  The
+    // ReLU masks of the backward pass are read back from the stored activations:
+    // 1[z_{k-1} > 0] = 1[h_k > 0] (h_k = ReLU(z_{k-1}) rounded to fp16; only 0 < z < 2^-25
+    // rounds to h = 0, below the fp16 MLP's own rounding of z), and from hH for the last layer
     float hH[32];
     for (int k = 0; k < H; ++k) {
       const int in = net.in_dim[k];
@@ -218,19 +220,15 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
       tmem_ld16(tmem + lane_base + cb, z);
       tmem_ld16(tmem + lane_base + cb + 16, z + 16);
       tmem_wait_ld();
-      uint32_t mk = 0;
+      const float cap = valid ? INFINITY : 0.f;   // padding rows: h = 0
 #pragma unroll
       for (int n = 0; n < 32; n += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + cb + n);
-        const float v[4] = {z[n] + b4.x, z[n + 1] + b4.y, z[n + 2] + b4.z, z[n + 3] + b4.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool pos = v[q] > 0.f && valid;
-          mk |= (uint32_t)pos << (n + q);
-          z[n + q] = pos ? v[q] : 0.f;
-        }
+        z[n] = fmaxf(fminf(z[n] + b4.x, cap), 0.f);
+        z[n + 1] = fmaxf(fminf(z[n + 1] + b4.y, cap), 0.f);
+        z[n + 2] = fmaxf(fminf(z[n + 2] + b4.z, cap), 0.f);
+        z[n + 3] = fmaxf(fminf(z[n + 3] + b4.w, cap), 0.f);
       }
-      mask[k] = mk;
       if (k + 1 < H) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], r, hf * 4 + j, z + 8 * j);
@@ -296,7 +294,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
         float a = 0.f;
 #pragma unroll
         for (int c = 0; c < D; ++c) a = fmaf(dy[c] * loss_scale, wout[c * 64 + cb + n], a);
-        dz[n] = ((mask[H - 1] >> n) & 1u) ? a : 0.f;
+        dz[n] = hH[n] > 0.f ? a : 0.f;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dz + 8 * j);
@@ -345,11 +343,23 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
         tmem_ld16(tmem + lane_base + cb + 16, dh + 16);
         tmem_wait_ld();
         if (k > 0) {
+          // dz_{k-1} = dh_k * 1[h_k > 0] on packed fp16 pairs (the mask multiplies by 1 or 0)
+          const uint8_t* hrow = smem + lay.h[k] + (r & 7) * 16 + (r >> 3) * lay.h_sbo[k];
+          uint8_t* drow = smem + (((H - k) & 1) ? lay.dz2 : lay.dz) + (r & 7) * 16 + (r >> 3) * lay.dz_sbo;
+          const __half2 zero2 = __float2half2_rn(0.f);
 #pragma unroll
-          for (int n = 0; n < 32; ++n) dh[n] = ((mask[k - 1] >> n) & 1u) ? dh[n] : 0.f;
+          for (int j = 0; j < 4; ++j) {
+            uint4 hv = *reinterpret_cast<const uint4*>(hrow + (hf * 4 + j) * 128);
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+            uint32_t o[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_row8(smem + (((H - k) & 1) ? lay.dz2 : lay.dz), lay.dz_sbo, r, hf * 4 + j, dh + 8 * j);
+            for (int p = 0; p < 4; ++p) {
+              const __half2 h2 = *reinterpret_cast<const __half2*>(&hw[p]);
+              __half2 d2 = __hmul2(__floats2half2_rn(dh[8 * j + 2 * p], dh[8 * j + 2 * p + 1]), __hgt2(h2, zero2));
+              o[p] = *reinterpret_cast<uint32_t*>(&d2);
+            }
+            *reinterpret_cast<uint4*>(drow + (hf * 4 + j) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
         } else if (valid) {
           // dfeat, unscaled, level-major (coalesced across the tile)
 #pragma unroll
