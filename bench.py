@@ -40,6 +40,9 @@ def parse():
     p.add_argument("--precision", default="fp16", choices=["fp16", "fp32"])
     p.add_argument("--psnr-steps", type=int, default=2000, help="total fit steps before the PSNR report (0: skip)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 strong-scaling sub-measurement")
+    p.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"],
+                   help="headline workload: cfg2 (weak scaling, default) or cfg3 (64 blocks split over the ranks)")
     return p.parse_args()
 
 
@@ -81,6 +84,73 @@ def oracle_step_sample(steps, warmup, frac=0.25):
     desc = (f"{steps} oracle fit steps (after {warmup} warm-up) of one 128^3 cfg2 block at {bu}+{bb} "
             f"coords/step ({frac / 8:.4f} of a cfg2 step), numpy fp64, 1 thread")
     return coords / dt, 1, desc
+
+
+_PAR_VOL = None   # the cfg2 volume, shared with the forked oracle workers
+
+
+def _oracle_block_worker(args):
+    """One process: one fit step sample of one cfg2 block (1 BLAS thread)."""
+    block_id, steps, frac = args
+    from threadpoolctl import threadpool_limits
+    from oracle import fit as o_fit, sampler
+    from oracle.model import Config, InrModel
+    vol = _PAR_VOL
+    lo, hi = float(vol.min()), float(vol.max())
+    blk = sampler.decompose((SIDE,) * 3, (BLOCK,) * 3)[block_id]
+    bu, bb = int(B_U * frac), int(B_B * frac)
+    with threadpool_limits(1):
+        m = InrModel(Config(**CFG), blk, 1)
+        opts = o_fit.FitOpts(vmin=lo, vmax=hi, boundary_batch=bb)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o_fit.train_step(m, vol, opts, bu)
+        return steps * (bu + bb), time.perf_counter() - t0
+
+
+def oracle_parallel_sample(steps=2, frac=0.25):
+    """SURVEY §8(d) "min(nproc, blocks) threads": one process per cfg2 block (8
+    blocks), each the oracle on one core.  Returns (coords/s over the slowest
+    worker's time, workers, description)."""
+    import multiprocessing as mp
+    import synth
+    global _PAR_VOL
+    _PAR_VOL = synth.g2_energy(SIDE).numpy()
+    n = max(1, min(os.cpu_count() or 1, 8))
+    ctx = mp.get_context("fork")   # the workers inherit the volume; they never touch CUDA
+    with ctx.Pool(n) as pool:
+        res = pool.map(_oracle_block_worker, [(b, steps, frac) for b in range(8)])
+    # 8 blocks over n workers: wall time ~ ceil(8 / n) x the per-block time
+    per_block = max(t for _, t in res)
+    coords = sum(c for c, _ in res)
+    wall = per_block * ((8 + n - 1) // n)
+    desc = (f"{steps} oracle fit steps of each of the 8 cfg2 blocks at {int(B_U * frac)}+{int(B_B * frac)} "
+            f"coords/step, one process per block on {n} cores (numpy fp64, 1 BLAS thread each); "
+            f"wall = ceil(8/{n}) x slowest block")
+    return coords / wall, n, desc
+
+
+def oracle_cfg1_full():
+    """cfg1 timed in full: 200 fit steps of the 64^3 G1 block at
+    B_u = 4096 + a 64^3 decode, the oracle on one core."""
+    from threadpoolctl import threadpool_limits
+    import synth
+    from oracle import decode as o_decode, fit as o_fit, sampler
+    from oracle.model import Config, InrModel
+    vol = synth.g1_analytic(64).numpy()
+    lo, hi = float(vol.min()), float(vol.max())
+    blk = sampler.decompose((64,) * 3, (64,) * 3)[0]
+    with threadpool_limits(1):
+        m = InrModel(Config(levels=8, features=2, log2_table_size=14, mlp_hidden_layers=2), blk, 1)
+        t0 = time.perf_counter()
+        o_fit.fit(m, vol, 200, 4096, o_fit.FitOpts(vmin=lo, vmax=hi))
+        t1 = time.perf_counter()
+        o_decode.decode_grid(m, (64, 64, 64))
+        t2 = time.perf_counter()
+    return {"fit_s": t1 - t0, "fit_coords_per_s": 200 * 4096 / (t1 - t0), "decode_s": t2 - t1,
+            "decode_voxels_per_s": 64 ** 3 / (t2 - t1), "cores": 1,
+            "sample": "cfg1 in full: 200 fit steps of the 64^3 G1 block (B_u = 4096, B_b = 0, L8 T2^14 F2 2x64) "
+                      "and its 64^3 grid decode, numpy fp64 oracle, 1 thread"}
 
 
 def run_reference(args):
@@ -162,28 +232,47 @@ class Clocks:
                 "samples_total": n_all}
 
 
-def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` from the
-    committed ncu --set full capture (profiles/), in bytes, or None."""
-    name = {"adam": "adam_kernel", "mlp_tc": "mlp_fit_kernel", "encode_bwd": "encode_bwd_kernel",
-            "encode_fwd": "encode_fwd_kernel"}.get(kernel, kernel)
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_final_ncu_full.txt")
+NCU_CAPTURE = "profiles/r2_ncu_full.txt"
+
+
+def ncu_capture():
+    """Per-kernel figures of one launch each from the committed ncu --set full
+    capture (profiles/r2_ncu_full.txt, tools/ncu_summary.py format): DRAM bytes,
+    L2 read / red sectors.  {bench kernel class: {...}}."""
+    names = {"step_begin": "step_begin_kernel", "encode_fwd": "encode_fwd_kernel", "prep_image": "prep_image_kernel",
+             "mlp_tc": "mlp_fit_kernel", "encode_bwd": "encode_bwd_kernel", "adam": "adam_kernel"}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    out, cur = {}, None
     try:
-        blk = None
-        for line in open(path):
+        for line in open(os.path.join(ROOT, NCU_CAPTURE)):
             if line.startswith("["):
-                blk = line.strip()
-            elif blk and name in blk and line.strip().startswith("traffic (read+write)"):
-                val, unit = float(line.split()[-2]), line.split()[-1]
-                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
-                return val * scale, os.path.relpath(path, os.path.dirname(path) + "/..") + \
-                    " (ncu --set full, one launch)"
+                k = line.strip()[1:-1]
+                cur = next((c for c, n in names.items() if n in k), None)
+                if cur:
+                    out.setdefault(cur, {})
+                continue
+            f = line.split()
+            if not cur or len(f) < 2:
+                continue
+            if line.strip().startswith("traffic (read+write)"):
+                out[cur]["dram_bytes"] = float(f[-2]) * scale.get(f[-1], 1.0)
+            elif f[0] == "lts__t_sectors_srcunit_tex_op_read.sum":
+                out[cur]["l2_read_sectors"] = float(f[1])
+            elif f[0] == "lts__t_sectors_srcunit_tex_op_red.sum":
+                out[cur]["l2_red_sectors"] = float(f[1])
     except OSError:
         pass
-    return None
+    return out
 
 
 # ------------------------------------------------------------------- our arm
+_T0 = time.time()
+
+
+def _phase(name):
+    print(f"[bench {time.time() - _T0:7.1f} s] {name}", file=sys.stderr, flush=True)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -220,15 +309,17 @@ def run_ours(args):
     nb = len(d.models)
     coords_per_step = nb * (B_U + B_B)
 
+    _phase('setup done')
     # warm-up (untimed)
     d.fit(vol, max(args.warmup, 1), B_U, opts, stream, report=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    # ---- timed region: K fit steps, every kernel bracketed by CUDA events
+    # ---- timed region (the production path: one captured CUDA graph per step,
+    # replayed K times; no profiling): K fit steps between two CUDA events on the
+    # launching stream, barrier + synchronize on both sides, max over ranks
     launches0 = inr.inr_kernel_launches()
-    inr.inr_profile_enable(1)
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.5)   # nvidia-smi start-up: its first samples land before the timed region
@@ -236,68 +327,111 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0.record()
     t_host0 = time.time()
+    ev0.record()
     d.fit(vol, args.steps, B_U, opts, stream, report=False)
     ev1.record()
     torch.cuda.synchronize()
     t_host1 = time.time()
     if world > 1:
         dist.barrier()
-    ms_outer = ev0.elapsed_time(ev1)            # includes the host-side graph capture of the K steps
-    ms = inr.inr_profile_span()                 # device time: first kernel start -> last kernel end
-    clk = clocks.stop(t_host0, t_host1)
     launches = inr.inr_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    ms_max = dnr.allreduce_max(ms)
+    value = coords_per_step * world * args.steps / (ms_max / 1e3)
+    # the same K-step call repeated 10 times (outside the contract's timed region): median
+    reps = []
+    for _ in range(10):
+        ev0.record()
+        d.fit(vol, args.steps, B_U, opts, stream, report=False)
+        ev1.record()
+        torch.cuda.synchronize()
+        reps.append(dnr.allreduce_max(ev0.elapsed_time(ev1)))
+    clk = clocks.stop(t_host0, time.time())
+    reps.sort()
+    ms_med = reps[len(reps) // 2]
+
+    # ---- per-kernel device times: a separate profiled K-step run (every library
+    # kernel bracketed by CUDA events on its stream, the K steps captured as one graph)
+    inr.inr_profile_enable(1)
+    d.fit(vol, args.steps, B_U, opts, stream, report=False)
+    torch.cuda.synchronize()
+    prof_span = inr.inr_profile_span()
     prof = {k: inr.inr_profile_read(k)
             for k in ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "fit_fp32", "adam")}
     inr.inr_profile_enable(0)
-    ms_max = dnr.allreduce_max(ms)
-    value = coords_per_step * world * args.steps / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel (device time share)
+    # ---- roofline of the dominant kernel and of the whole step
     P = inr.inr_param_count(d.models[0])
+    P_int = P   # (the declared count; the internal 64-float padding adds < 0.1%)
     pk, pv = peaks()
     kern = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms, dom_n = kern[dom]
     avg_s = dom_ms / dom_n / 1e3
+    LF, W, H = CFG["levels"] * CFG["features"], 64, CFG["mlp_hidden_layers"]
     if dom == "adam":
-        # algorithmic bytes: read p, g, m, v + write p, m, v (fp32) for every parameter of every block
-        alg = 28.0 * P * nb
+        # algorithmic bytes: read p, g, m, v + write p, m, v (fp32) for every parameter of
+        # every block = 28 B/param (the gradient is zeroed by encode_fwd, charged there)
+        alg = 28.0 * P_int * nb
         roof = {"kernel": "adam", "bound": "hbm", "achieved": alg / avg_s / 1e9, "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": alg}
+                "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": alg,
+                "convention": "28 B/param/step (p, g, m, v read; p, m, v written); the 4 B/param gradient "
+                              "zeroing runs inside encode_fwd and is charged to the whole step below"}
     else:
-        # the fused fit kernel: the dense contraction part on the tensor roofline
-        # (6 (LF W + (H-1) W^2 + W) FLOP per coordinate), plus its
-        # algorithmic L2 gather/scatter bytes (2 x 8 L F 4 B per coordinate)
-        LF, W, H = 32, 64, 3
         flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step
-        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])  # fp16 dense rate == bf16 on B200
+        peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
         roof = {"kernel": dom, "bound": "tensor", "achieved": flop / avg_s / 1e12, "peak": peak,
-                "unit": "TFLOP/s", "traffic": None, "algorithmic_flop_per_launch": flop,
-                "l2_gather_scatter_bytes_per_launch": 2 * 8 * 16 * 2 * 4.0 * coords_per_step}
+                "unit": "TFLOP/s", "traffic": None, "algorithmic_flop_per_launch": flop}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    tr = ncu_traffic(roof["kernel"])
-    if tr is not None:
-        roof["traffic"], roof["traffic_source"] = tr
+    ncu = ncu_capture()
+    if dom in ncu:
+        roof["traffic"] = ncu[dom]["dram_bytes"]
+        roof["traffic_source"] = NCU_CAPTURE + " (ncu --set full, one launch, cold L2)"
     roof["peak_source"] = pv
     roof["avg_launch_ms"] = avg_s * 1e3
-    roof["share_of_step"] = dom_ms / ms
+    roof["share_of_step"] = dom_ms / prof_span
     kernels = {k: {"total_ms": v[0], "launches": v[1], "avg_ms": v[0] / max(v[1], 1)} for k, v in kern.items()}
-    # the gather / scatter kernels against the measured random-access peaks (tools/l2_peaks.py)
-    try:
+    # per-kernel fractions against each kernel's own bound
+    flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step
+    if "mlp_tc" in kernels:
+        tf = flop / (kernels["mlp_tc"]["avg_ms"] / 1e3) / 1e12
+        kernels["mlp_tc"].update({"bound": "tensor", "achieved_tflops": tf,
+                                  "peak_tflops": pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+                                  "frac": tf / pk.get("bf16_tflops_sustained", pk["bf16_tflops"])})
+    try:   # gather / red kernels: L2 sectors per launch (ncu capture) / avg launch vs the measured peaks
         with open(os.path.join(ROOT, "profiles", "r1_l2_peaks.json")) as f:
             lp = {(r["op"], r["buffer_MB"]): r["per_s"] for r in json.load(f)["results"]}
-        corners = 8.0 * CFG["levels"] * coords_per_step
-        for k, op in (("encode_fwd", "gather_16B"), ("encode_bwd", "red_v4_f32")):
-            if k in kernels:
-                rate = corners / (kernels[k]["avg_ms"] / 1e3)
-                kernels[k].update({"corner_accesses_per_s": rate, "random_access_peak_per_s": lp[(op, 4)],
-                                   "peak_note": f"{op}, 4 MB L2-resident buffer, measured; x-neighbour corner "
-                                                "pairs share one access, so corners/s can exceed the access peak"})
+        for k, op, key in (("encode_fwd", "gather_16B", "l2_read_sectors"), ("encode_bwd", "red_v4_f32", "l2_red_sectors")):
+            if k in kernels and k in ncu and ncu[k].get(key):
+                rate = ncu[k][key] / (kernels[k]["avg_ms"] / 1e3)
+                kernels[k].update({"bound": "l2 random access", "l2_sectors_per_launch": ncu[k][key],
+                                   "achieved_sectors_per_s": rate, "peak_accesses_per_s": lp[(op, 64)],
+                                   "frac": rate / lp[(op, 64)],
+                                   "peak_note": f"{op} on a 64 MB L2-resident buffer (profiles/r1_l2_peaks.json); "
+                                                "sector counts from " + NCU_CAPTURE})
     except (OSError, KeyError, ValueError):
         pass
+    if "adam" in kernels:
+        kernels["adam"].update({"bound": "hbm", "frac": 28.0 * P_int * nb / (kernels["adam"]["avg_ms"] / 1e3) / 1e9
+                                / pk["hbm_gbs"]})
+    # whole step: the algorithmic HBM bytes of one step (Adam 28 B/param + gradient zeroing
+    # 4 B/param + 8 texels of 4 B per coordinate) over the measured step time, and the
+    # DRAM traffic the ncu capture saw per step against that
+    alg_step = 32.0 * P_int * nb + 32.0 * coords_per_step
+    step_s = ms_max / args.steps / 1e3
+    whole = {"bound": "hbm", "algorithmic_bytes": alg_step, "achieved_gbs": alg_step / step_s / 1e9,
+             "peak_gbs": pk["hbm_gbs"], "frac": alg_step / step_s / 1e9 / pk["hbm_gbs"],
+             "note": "whole fit step: Adam 28 B/param + zeroing 4 B/param + texels 32 B/coordinate over the "
+                     "production step time; the L2-bound encode/scatter and the tensor-core MLP add time but "
+                     "no algorithmic HBM bytes"}
+    fit_k = ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "adam")
+    if all(k in ncu for k in fit_k):
+        dram = sum(ncu[k]["dram_bytes"] for k in fit_k)
+        whole.update({"dram_bytes_per_step": dram, "dram_over_algorithmic": dram / alg_step,
+                      "dram_source": NCU_CAPTURE + " (sum over the step's kernels, each with a cold L2)"})
 
+    _phase('timed fit + profile done')
     # ---- end to end through the public API with host buffers: every step the
     # volume is copied H2D from pinned memory, one fit step runs through
     # inr_fit_group, and its losses come back to the host (inr_fit_losses -> D2H)
@@ -358,6 +492,7 @@ def run_ours(args):
                        "copied D2H and read on the host while the next step runs",
            "last_loss_uniform_mean": losses[-1]}
 
+    _phase('e2e done')
     # ---- decode throughput (1x grid of the local cores) and PSNR @ ratio
     out = torch.empty_like(vol)
     sse = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -431,6 +566,7 @@ def run_ours(args):
     raw_bytes = 4.0 * SIDE ** 3
     ratio = raw_bytes / d.param_bytes()
 
+    _phase('decode + psnr done')
     # ---- NEXT-3: sort-last direct-query volume rendering of the trained DNR (1024^2)
     W = H = 1024
     cam = inr.make_camera((-180.0, 330.0, -260.0 * world), (128.0, 110.0, 128.0 * world), (0.0, 1.0, 0.0), 34.0, W, H)
@@ -457,32 +593,148 @@ def run_ours(args):
         render["mean_alpha"] = float(img[:, 3].mean())
     del img
 
+    _phase('render done')
+    # ---- cfg3: 64 blocks of a 512^3 volume split over the ranks
+    d.close()
+    del vol, out, bufs, host
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    cfg3 = None
+    if not args.no_cfg3 or args.config == "cfg3":
+        cfg3 = run_cfg3(args, world, rank, local, dev, stream, cfg)
+
+    _phase('cfg3 done')
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, desc = oracle_step_sample(2, 0)
         cpu = {"value": v, "unit": "coords/s", "cores": cores, "kind": "oracle", "sample": desc,
-               "cpu": _cpu_model()}
+               "cpu": _cpu_model(), "nproc": os.cpu_count()}
+        pv_, pn_, pd_ = oracle_parallel_sample()
+        cpu["parallel"] = {"value": pv_, "unit": "coords/s", "cores": pn_, "kind": "oracle", "sample": pd_}
+        cpu["cfg1_full"] = oracle_cfg1_full()
+    _phase('cpu baseline done')
     if rank == 0:
         line = {
             "metric": "fit_coords_per_s", "value": value, "unit": "coords/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "timing": "CUDA events on the launching stream around every library kernel of the K steps "
-                      "(one captured CUDA graph); ms = first kernel start -> last kernel end, max over ranks",
-            "host_capture_ms": ms_outer - ms,
+            "ms_per_step_median_of_10": ms_med / args.steps,
+            "timing": "production path (one captured CUDA graph per step, replayed K times): CUDA events on the "
+                      "launching stream around the K-step inr_fit_group call, barrier + synchronize on both sides, "
+                      "max over ranks; the median is over 10 more identical K-step calls; per-kernel times come "
+                      "from a separate profiled K-step run",
+            "profiled_span_ms_per_step": prof_span / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f16-mlp/f32" if prec else "f32", "data": "synthetic",
             "config": workload_config(world, args),
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "whole_step_roofline": whole, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "decode": decode, "render": render, "psnr_db": psnr, "psnr_block_min_db": psnr_block_min,
             "psnr_after_steps": done,
             "compression_ratio": ratio,
             "clocks": clk, "gpu_launches": launches,
+            "cfg3_strong": cfg3,
         }
+        if args.config == "cfg3" and cfg3 and "value" in cfg3:
+            # cfg3 headline: 64 blocks of the 512^3 volume split over the ranks (strong scaling)
+            cfg2_line = {k: line[k] for k in ("value", "ms_per_step", "ms_per_step_median_of_10", "config", "e2e",
+                                              "roofline", "whole_step_roofline", "kernels", "decode")}
+            for k in ("e2e", "roofline", "whole_step_roofline", "kernels", "decode", "cfg3_strong",
+                      "ms_per_step_median_of_10"):
+                line.pop(k, None)
+            line.update({"value": cfg3["value"], "ms_per_step": cfg3["ms_per_step"], "scaling": "strong",
+                         "config": cfg3["config"], "decode": cfg3["decode"], "gpu_launches": cfg3["gpu_launches"],
+                         "e2e": cfg3["e2e"], "cfg2_weak": cfg2_line})
         print(json.dumps(line), flush=True)
-    d.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_cfg3(args, world, rank, local, dev, stream, cfg):
+    """cfg3: G3 512^3, 4x4x4 blocks of 128^3 split over the ranks in contiguous
+    z-major ranges (64/N blocks each, strong scaling); cfg2's network and batch.
+    K production fit steps timed like the headline (max over ranks), plus the 1x
+    grid decode of the rank's blocks and an end-to-end K-step fit through the
+    public API with the rank's sub-volume copied H2D from pinned memory."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2304_10516_b200 import dnr, inr
+    g3 = (512, 512, 512)
+    try:
+        d = dnr.DNR(g3, (BLOCK,) * 3, cfg, rank, world, local)
+    except ValueError as e:
+        return {"unavailable": str(e)}
+    lo, hi = d.lo, d.hi
+    vol = torch.empty((hi[2] - lo[2] + 1, hi[1] - lo[1] + 1, hi[0] - lo[0] + 1), dtype=torch.float32, device=dev)
+    for z0 in range(0, vol.shape[0], 8):
+        z1 = min(z0 + 8, vol.shape[0])
+        pos = synth.lattice(g3, dev, (lo[2] + z0, lo[2] + z1))[:, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+        vol[z0:z1] = synth.evaluate("g3", pos, g3).to(torch.float32)
+    d.value_range(vol, stream)
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = B_B
+    nb = len(d.models)
+    d.fit(vol, max(args.warmup, 3), B_U, opts, stream, report=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = inr.inr_kernel_launches()
+    e0.record()
+    d.fit(vol, args.steps, B_U, opts, stream, report=False)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = inr.inr_kernel_launches() - l0
+    if world > 1:
+        dist.barrier()
+    ms = dnr.allreduce_max(e0.elapsed_time(e1))
+    coords = 64 * (B_U + B_B) * args.steps
+    # end to end: the rank's sub-volume H2D from pinned memory every step, one step per call,
+    # the loss report D2H (as the headline's e2e, without the double buffering)
+    host = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
+    host.copy_(vol)
+    buf = torch.empty_like(vol)
+    rep_dev = torch.empty(3 * nb, dtype=torch.float64, device=dev)
+    rep_host = torch.empty(3 * nb, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        buf.copy_(host, non_blocking=True)
+        d.fit(buf, 1, B_U, opts, stream, report=False)
+        inr.inr_fit_losses(d.models, rep_dev.data_ptr(), stream)
+        rep_host.copy_(rep_dev, non_blocking=True)
+    torch.cuda.synchronize()
+    e2e_s = dnr.allreduce_max(time.perf_counter() - t0)
+    # 1x grid decode of the rank's blocks
+    out = torch.empty_like(vol)
+    d.decode_grid_local(out, 1, None, None, stream)
+    torch.cuda.synchronize()
+    e0.record()
+    d.decode_grid_local(out, 1, None, None, stream)
+    e1.record()
+    torch.cuda.synchronize()
+    dec_ms = dnr.allreduce_max(e0.elapsed_time(e1))
+    res = {"value": coords / (ms / 1e3), "unit": "coords/s", "ms_per_step": ms / args.steps, "steps": args.steps,
+           "scaling": "strong", "blocks_per_rank": nb, "gpu_launches": launches,
+           "config": {"workload": "cfg3: G3 512^3 cosmology-density-shaped, 4x4x4 blocks of 128^3 split over the "
+                                  "ranks (contiguous z-major ranges), L16 T2^19 F2, 3x64 MLP, 65536+16384 "
+                                  "coords/block/step", "global_dims": list(g3), "blocks": 64,
+                      "blocks_per_gpu": nb, "parallelism": f"blocks{world}" if world > 1 else "single",
+                      "l2": "no flush: working set (params+grads+Adam state 195 MB/block) >> 126 MB L2"},
+           "e2e": {"value": coords / e2e_s, "unit": "coords/s", "h2d_bytes_per_step": int(vol.numel() * 4),
+                   "d2h_bytes_per_step": int(3 * nb * 8),
+                   "clock": "host wall clock around K steps (sub-volume H2D from pinned memory, one fit step, "
+                            "loss report D2H per step), max over ranks"},
+           "decode": {"voxels_per_s": 512 ** 3 / (dec_ms / 1e3), "ms": dec_ms, "voxels": 512 ** 3}}
+    d.close()
+    del vol, out, buf, host
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
 
 
 def _cpu_model():

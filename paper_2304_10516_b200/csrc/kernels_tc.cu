@@ -112,8 +112,25 @@ __device__ __forceinline__ void mlp_teardown(uint32_t tmem, const Layout& lay) {
 // warps hide the MMA and TMEM latencies.  featimg: fp16 h_0 tile images,
 // samples: float4 (x, y, z, target); writes dfeat fp32 [model][level][Bs][F];
 // adds dW, db into the model's gradient.
-constexpr int kFitThreads = 256;
+constexpr int kFitQ = 2;                      // threads per tile row (column groups of 64 / kFitQ)
+constexpr int kFitCW = 64 / kFitQ;              // columns per thread
+constexpr int kFitThreads = kTileM * kFitQ;
 constexpr int kDetCtasPerModel = 32;   // deterministic mode: MLP CTAs per model, independent of the group
+
+// Sum 16 per-lane values over the warp; lanes l and l + 16 end with the sum of column l.
+__device__ __forceinline__ float warp_transpose_reduce16(float* v, int lane) {
+#pragma unroll
+  for (int half = 8, off = 8; off >= 1; half >>= 1, off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < half; ++j) {
+      float keep = up ? v[j + half] : v[j];
+      float send = up ? v[j] : v[j + half];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
 
 // Sum 32 per-lane values over the warp; lane l ends with the sum of column l.
 __device__ __forceinline__ float warp_transpose_reduce32(float* v, int lane) {
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
   const int m = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int r = t & (kTileM - 1), hf = t >> 7, cb = hf * 32;   // row, column half
+  const int r = t & (kTileM - 1), q = t >> 7, cb = q * kFitCW;   // row, column group
   const int H = net.H, L = net.L, ones = lay.ones;
   const int B_b = md.nfaces > 0 ? fs.B_b : 0;
   const int total = fs.B_u + B_b;
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
   // point in the deterministic mode (the warps add in a run-dependent order)
   float* red = reinterpret_cast<float*>(smem + lay.red);
   unsigned long long* redx = reinterpret_cast<unsigned long long*>(smem + lay.red);
-  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [D][2][128] output-layer partial sums
+  float* ypart = reinterpret_cast<float*>(smem + lay.ypart);   // [D][kFitQ][128] output-layer partial sums
   const uint32_t mbar = smem_u32(smem + lay.mbar);
   for (int i = t; i < D * 65; i += kFitThreads) redx[i] = 0ull;
   const uint32_t tmem = mlp_setup_fit(net, wimg + (size_t)m * lay.img_bytes, smem, lay);
@@ -200,11 +217,11 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
                fbar[b ^ 1]);
     }
     mbar_wait(fbar[b], (uint32_t)(it >> 1) & 1u);
-    // ---- forward through the hidden layers (this thread: columns [cb, cb + 32)).  The
+    // ---- forward through the hidden layers (this thread: columns [cb, cb + kFitCW)).  The
     // ReLU masks of the backward pass are read back from the stored activations:
     // 1[z_{k-1} > 0] = 1[h_k > 0] (h_k = ReLU(z_{k-1}) rounded to fp16; only 0 < z < 2^-25
     // rounds to h = 0, below the fp16 MLP's own rounding of z), and from hH for the last layer
-    float hH[32];
+    float hH[kFitCW];
     for (int k = 0; k < H; ++k) {
       const int in = net.in_dim[k];
       if (t == 0) {
@@ -216,13 +233,13 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
       mbar_wait(mbar, phase);
       phase ^= 1;
       fence_after();
-      float z[32];
-      tmem_ld16(tmem + lane_base + cb, z);
-      tmem_ld16(tmem + lane_base + cb + 16, z + 16);
+      float z[kFitCW];
+#pragma unroll
+      for (int c = 0; c < kFitCW; c += 16) tmem_ld16(tmem + lane_base + cb + c, z + c);
       tmem_wait_ld();
       const float cap = valid ? INFINITY : 0.f;   // padding rows: h = 0
 #pragma unroll
-      for (int n = 0; n < 32; n += 4) {
+      for (int n = 0; n < kFitCW; n += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + cb + n);
         z[n] = fmaxf(fminf(z[n] + b4.x, cap), 0.f);
         z[n + 1] = fmaxf(fminf(z[n + 1] + b4.y, cap), 0.f);
@@ -231,19 +248,20 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
       }
       if (k + 1 < H) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], r, hf * 4 + j, z + 8 * j);
+        for (int j = 0; j < kFitCW / 8; ++j)
+          st_row8(smem + lay.h[k + 1], lay.h_sbo[k + 1], r, q * (kFitCW / 8) + j, z + 8 * j);
       } else {
         float yp[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) yp[c] = 0.f;
 #pragma unroll
-        for (int n = 0; n < 32; ++n) {
+        for (int n = 0; n < kFitCW; ++n) {
           hH[n] = z[n];
 #pragma unroll
           for (int c = 0; c < D; ++c) yp[c] = fmaf(wout[c * 64 + cb + n], z[n], yp[c]);
         }
 #pragma unroll
-        for (int c = 0; c < D; ++c) ypart[(2 * c + hf) * kTileM + r] = yp[c];
+        for (int c = 0; c < D; ++c) ypart[(kFitQ * c + q) * kTileM + r] = yp[c];
       }
       fence_async_smem();
       fence_before();
@@ -254,13 +272,15 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
     double ad = 0.0;
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      const float y = wout[D * 64 + c] + ypart[(2 * c) * kTileM + r] + ypart[(2 * c + 1) * kTileM + r];
+      float y = wout[D * 64 + c];
+#pragma unroll
+      for (int p = 0; p < kFitQ; ++p) y += ypart[(kFitQ * c + p) * kTileM + r];
       const float d = y - target[c];
       const float sg = valid ? (d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f)) : 0.f;
       dy[c] = is_b ? lam * sg / (float)(max(B_b, 1) * D) : (1.f - lam) * sg / (float)(fs.B_u * D);
       ad += fabs((double)d);
     }
-    if (hf == 0) {
+    if (q == 0) {
       double au = (valid && !is_b) ? ad : 0.0;
       double ab = (valid && is_b) ? ad : 0.0;
 #pragma unroll
@@ -281,23 +301,28 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
       }
     }
 #pragma unroll
-    for (int c = 0; c < D; ++c) {   // dW_H[c][n] = sum_s dy_c,s h_H[s][n] for this thread's 32 columns
-      float v[32];
+    for (int c = 0; c < D; ++c) {   // dW_H[c][n] = sum_s dy_c,s h_H[s][n] for this thread's columns
+      float v[kFitCW];
 #pragma unroll
-      for (int n = 0; n < 32; ++n) v[n] = dy[c] * hH[n];
-      red_smem(red, redx, det, c * 64 + cb + lane, warp_transpose_reduce32(v, lane));
+      for (int n = 0; n < kFitCW; ++n) v[n] = dy[c] * hH[n];
+      if constexpr (kFitCW == 32) {
+        red_smem(red, redx, det, c * 64 + cb + lane, warp_transpose_reduce32(v, lane));
+      } else {
+        const float sv = warp_transpose_reduce16(v, lane);
+        if (lane < 16) red_smem(red, redx, det, c * 64 + cb + lane, sv);
+      }
     }
     {   // dz_{H-1} = (sum_c dy_c W_H[c]) * 1[z_{H-1} > 0], scaled by 2^s
-      float dz[32];
+      float dz[kFitCW];
 #pragma unroll
-      for (int n = 0; n < 32; ++n) {
+      for (int n = 0; n < kFitCW; ++n) {
         float a = 0.f;
 #pragma unroll
         for (int c = 0; c < D; ++c) a = fmaf(dy[c] * loss_scale, wout[c * 64 + cb + n], a);
         dz[n] = hH[n] > 0.f ? a : 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, hf * 4 + j, dz + 8 * j);
+      for (int j = 0; j < kFitCW / 8; ++j) st_row8(smem + lay.dz, lay.dz_sbo, r, q * (kFitCW / 8) + j, dz + 8 * j);
     }
     fence_async_smem();
     fence_before();
@@ -337,10 +362,10 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
       mbar_wait(mbar, phase);
       phase ^= 1;
       fence_after();
-      if (cb < in) {   // warp-uniform: this half has columns of dh
-        float dh[32];
-        tmem_ld16(tmem + lane_base + cb, dh);
-        tmem_ld16(tmem + lane_base + cb + 16, dh + 16);
+      if (cb < in) {   // warp-uniform: this group has columns of dh
+        float dh[kFitCW];
+#pragma unroll
+        for (int c = 0; c < kFitCW; c += 16) tmem_ld16(tmem + lane_base + cb + c, dh + c);
         tmem_wait_ld();
         if (k > 0) {
           // dz_{k-1} = dh_k * 1[h_k > 0] on packed fp16 pairs (the mask multiplies by 1 or 0)
@@ -348,8 +373,8 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
           uint8_t* drow = smem + (((H - k) & 1) ? lay.dz2 : lay.dz) + (r & 7) * 16 + (r >> 3) * lay.dz_sbo;
           const __half2 zero2 = __float2half2_rn(0.f);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 hv = *reinterpret_cast<const uint4*>(hrow + (hf * 4 + j) * 128);
+          for (int j = 0; j < kFitCW / 8; ++j) {
+            uint4 hv = *reinterpret_cast<const uint4*>(hrow + (q * (kFitCW / 8) + j) * 128);
             const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
             uint32_t o[4];
 #pragma unroll
@@ -358,21 +383,21 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
               __half2 d2 = __hmul2(__floats2half2_rn(dh[8 * j + 2 * p], dh[8 * j + 2 * p + 1]), __hgt2(h2, zero2));
               o[p] = *reinterpret_cast<uint32_t*>(&d2);
             }
-            *reinterpret_cast<uint4*>(drow + (hf * 4 + j) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(drow + (q * (kFitCW / 8) + j) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         } else if (valid) {
           // dfeat, unscaled, level-major (coalesced across the tile)
 #pragma unroll
-          for (int c = 0; c < 32; c += F) {
+          for (int c = 0; c < kFitCW; c += F) {
             if (cb + c < net.LF) {
               float* o = dfeatm + ((size_t)((cb + c) / F) * Bs + i) * F;
               if constexpr (F == 1) { o[0] = dh[c] * inv_scale; }
               else if constexpr (F == 2) { *reinterpret_cast<float2*>(o) = make_float2(dh[c] * inv_scale, dh[c + 1] * inv_scale); }
               else {
 #pragma unroll
-                for (int q = 0; q < F; q += 4)
-                  *reinterpret_cast<float4*>(o + q) = make_float4(dh[c + q] * inv_scale, dh[c + q + 1] * inv_scale,
-                                                                  dh[c + q + 2] * inv_scale, dh[c + q + 3] * inv_scale);
+                for (int u = 0; u < F; u += 4)
+                  *reinterpret_cast<float4*>(o + u) = make_float4(dh[c + u] * inv_scale, dh[c + u + 1] * inv_scale,
+                                                                  dh[c + u + 2] * inv_scale, dh[c + u + 3] * inv_scale);
               }
             }
           }
@@ -391,8 +416,8 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
     for (int k = 0; k < H; ++k) {
       const int in = net.in_dim[k];
       const int ncol = in + ones;
-      // M = 64 accumulator: row 16q + l lives in lane 32q + l (l < 16); halves take alternate 16-column chunks
-      for (int c = hf * 16; c < ncol; c += 32) {
+      // M = 64 accumulator: row 16w + l lives in lane 32w + l (l < 16); groups take alternate 16-column chunks
+      for (int c = q * 16; c < ncol; c += 16 * kFitQ) {
         float v[16];
         tmem_ld16(tmem + lane_base + lay.col_dw[k] + c, v);
         tmem_wait_ld();
@@ -467,7 +492,7 @@ static bool build_layout(const NetDesc& net, Layout& L, bool train = true) {
   if (train) L.dz = take(kTileM * 64 * 2, 1024);
   if (train) L.dz2 = take(kTileM * 64 * 2, 1024);
   L.red = take((net.D * 65 + 1) * 8, 16);
-  L.ypart = take(net.D * 2 * kTileM * 4, 16);
+  L.ypart = take(net.D * 4 * kTileM * 4, 16);   // [D][<= 4 column groups][128]
   L.mbar = take(8, 8);
   L.mbar_img = take(8, 8);
   L.mbar_feat[0] = take(8, 8);
