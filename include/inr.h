@@ -164,7 +164,11 @@ INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
  *   cell-centred probe lattice reaches the target.
  *   Vector fields (out_dim 3) take per-channel ranges [vmin_c[c], vmax_c[c]]
  *   instead (vmin/vmax are then ignored); the L1 terms and the probe
- *   MSE pool over samples and channels [R28]. */
+ *   MSE pool over samples and channels [R28].
+ *   sparse_adam != 0 (default 0; NEXT-4, a flagged semantics change versus
+ *   R12, DESIGN R37): a hash-table parameter is updated only if its aligned
+ *   group of 8 table floats (one 32-B sector) received a non-zero gradient this
+ *   step; untouched groups keep p, m and v.  MLP parameters stay dense. */
 typedef struct {
   double lambda;
   int32_t boundary_batch;
@@ -175,6 +179,7 @@ typedef struct {
   double target_psnr;
   int32_t check_interval;
   double vmin_c[INR_MAX_CHANNELS], vmax_c[INR_MAX_CHANNELS];
+  int32_t sparse_adam;        /* R37: touched-only table updates (0 = dense PyTorch Adam) */
 } inr_fit_opts;
 INR_API void inr_fit_opts_default(inr_fit_opts* o);
 

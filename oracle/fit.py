@@ -29,6 +29,7 @@ class FitOpts:
     vmax: float = 1.0
     target_psnr: float = 0.0      # <= 0: fixed step count
     check_interval: int = 0
+    sparse_adam: int = 0          # R37 (NEXT-4 variant): touched-only table updates
 
 
 @dataclasses.dataclass
@@ -93,7 +94,11 @@ def train_step(model, volume, opts, batch):
     _, l1u, l1b, dy_u, dy_b = loss.loss_and_grad(yu, t_u, yb, t_b, opts.lam)
     dy = np.concatenate([dy_u, dy_b]).reshape(-1, D)
     model.g = gradients(model, x, dy, cache)
-    adam.adam_update(model.p, model.g, model.m, model.v, s + 1, lr, opts.beta1, opts.beta2, opts.eps)
+    if opts.sparse_adam:
+        tables = [(off, int(np.prod(shape))) for name, shape, off in model.cfg.tensor_layout() if name.startswith("table")]
+        adam.adam_update_sparse(model.p, model.g, model.m, model.v, s + 1, lr, tables, opts.beta1, opts.beta2, opts.eps)
+    else:
+        adam.adam_update(model.p, model.g, model.m, model.v, s + 1, lr, opts.beta1, opts.beta2, opts.eps)
     model.step += 1
     return l1u, l1b, const
 

@@ -540,6 +540,7 @@ extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
   for (int c = 0; c < INR_MAX_CHANNELS; ++c) { o->vmin_c[c] = 0.0; o->vmax_c[c] = 1.0; }
   o->target_psnr = 0.0;
   o->check_interval = 0;
+  o->sparse_adam = 0;
 }
 
 // Make sure device-resident parameters exist for a (possibly host-resident) model.
@@ -698,6 +699,8 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   as.ob1 = (float)(1.0 - opts->beta1);
   as.ob2 = (float)(1.0 - opts->beta2);
   as.eps = (float)opts->eps;
+  as.sparse = opts->sparse_adam != 0;
+  as.table_end = m0->net.w_off[0];   // tables: internal parameters [0, w_off[0])
 
   for (int i = 0; i < nmodels; ++i) {
     for (int c = 0; c < D; ++c) {

@@ -276,7 +276,10 @@ __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
   const ModelDev& md = g.md[blockIdx.y];
   const AdamStep a = adam_step_scalars(*md.step_cur, as.lr0, as.lr_decay, as.lr_step, as.beta1, as.beta2, as.b1,
                                        as.b2, as.ob1, as.ob2, as.eps);
-  const bool bad = adam_range(md, a, 0, g.net.nparams, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const bool bad = as.sparse ? adam_range_sparse(md, a, 0, as.table_end, tid, nth) |
+                                   adam_range(md, a, as.table_end, g.net.nparams, tid, nth)
+                             : adam_range(md, a, 0, g.net.nparams, tid, nth);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(md.flag, 1);
 }
 

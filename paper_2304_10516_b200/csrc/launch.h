@@ -25,6 +25,8 @@ struct AdamScalars {
   double lr0, lr_decay, beta1, beta2;
   long long lr_step;
   float b1, b2, ob1, ob2, eps;   // fp32 beta, 1 - beta (formed in fp64), eps
+  int sparse;                    // R37: touched-only table updates
+  long long table_end;           // internal offset where the MLP parameters start
 };
 
 constexpr int kMaxRouteBlocks = 4096;

@@ -355,6 +355,49 @@ def test_adam_elementwise_across_lr_decays(prec):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
+def test_sparse_adam_elementwise(prec):
+    """R37 (NEXT-4 touched-only Adam, opts.sparse_adam): each step's GPU
+    gradient fed to the oracle's adam_update_sparse (pinned in test_oracle_pins)
+    over 6 steps; table groups of 8 floats without a non-zero gradient keep p, m,
+    v bitwise on the GPU, the rest track the oracle to fp32 rounding.  A small
+    batch against T = 2^14 leaves most hashed-level groups untouched."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[3]
+    lo, hi = sampler.value_range([vol])
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch, go.sparse_adam = lo, hi, 64, 1
+    cfg = oracle_config(**CFG1)
+    tables = [(off, int(np.prod(shape))) for name, shape, off in cfg.tensor_layout() if name.startswith("table")]
+    vt = gpu_volume(vol)
+    m = make_gpu_model(blk, 8, reduction=1, precision=prec, **CFG1)
+    p = get_params(m).astype(np.float64)
+    mo, vo = np.zeros_like(p), np.zeros_like(p)
+    gmax = np.zeros_like(p)
+    untouched_seen = 0
+    for t in range(1, 7):
+        prev = get_params(m)
+        inr.inr_fit(m, whole_view(vt), 1, 256, go, stream())
+        g = get_grads(m).astype(np.float64)
+        gmax = np.maximum(gmax, np.abs(g))
+        o_adam.adam_update_sparse(p, g, mo, vo, t, 1e-2, tables)
+        pg = get_params(m)
+        mg, vg = inr.inr_get_adam_state(m, np.empty_like(pg), np.empty_like(pg))
+        keep = np.ones(p.shape, bool)
+        for off, n in tables:
+            keep[off:off + n] = ~o_adam.touched_groups(g[off:off + n])
+        keep[tables[-1][0] + tables[-1][1]:] = False
+        untouched_seen += int(keep.sum())
+        assert np.array_equal(pg[keep], prev[keep])            # untouched groups: bitwise unchanged
+        tol_p = t * (1e-6 * 1e-2 + 2.0 ** -21 * np.abs(p))
+        assert np.all(np.abs(pg - p) <= tol_p)
+        assert np.all(np.abs(mg - mo) <= t * 2.0 ** -21 * gmax + 1e-30)
+        assert np.all(np.abs(vg - vo) <= t * 2.0 ** -21 * vo + 1e-37)
+    print("prec", prec, "untouched parameter-steps", untouched_seen, "of", 6 * p.size)
+    assert untouched_seen > p.size        # the variant skipped a substantial part of the table
+    inr.inr_destroy(m)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
 def test_probe_psnr_matches_oracle(prec):
     """The stop check's probe PSNR ("until the user-defined accuracy
     criterion (such as a PSNR target)"): the GPU's 32^3 probe SSE, as

@@ -279,6 +279,37 @@ def test_adam_vs_torch_optim():
     assert np.allclose(p, tp.detach().numpy(), rtol=1e-14, atol=1e-15)
 
 
+def test_sparse_adam_groups():
+    """R37 (NEXT-4 touched-only Adam): a table group of 8 floats with no
+    non-zero gradient keeps p, m, v bitwise; a group with any non-zero entry,
+    and every MLP parameter, takes exactly the dense R12 update (pinned above
+    against torch.optim.Adam), zero-gradient members included; a ragged last
+    group counts as a group."""
+    rng = np.random.default_rng(12)
+    n_tab, n_mlp = 21, 5                      # groups [0,8), [8,16), [16,21)
+    p0, m0, v0 = rng.normal(size=26), rng.random(26) * 0.1, rng.random(26) * 0.01
+    g = np.zeros(26)
+    g[3] = 0.7                                # touches group 0 only
+    g[n_tab:] = 0.0                           # MLP gradients zero: still updated (m, v decay)
+    p, m, v = p0.copy(), m0.copy(), v0.copy()
+    adam.adam_update_sparse(p, g, m, v, 3, 1e-2, [(0, n_tab)])
+    pd, md, vd = p0.copy(), m0.copy(), v0.copy()
+    adam.adam_update(pd, g, md, vd, 3, 1e-2)
+    touched = np.r_[np.arange(0, 8), np.arange(n_tab, 26)]
+    untouched = np.arange(8, n_tab)
+    for a, b in ((p, pd), (m, md), (v, vd)):
+        assert np.array_equal(a[touched], b[touched])
+    for a, b in ((p, p0), (m, m0), (v, v0)):
+        assert np.array_equal(a[untouched], b[untouched])
+    assert not np.array_equal(m[n_tab:], m0[n_tab:])          # the MLP part moved with g = 0
+    g2 = rng.normal(size=26)                                     # every group touched: dense
+    p, m, v, pd, md, vd = p0.copy(), m0.copy(), v0.copy(), p0.copy(), m0.copy(), v0.copy()
+    adam.adam_update_sparse(p, g2, m, v, 1, 1e-2, [(0, n_tab)])
+    adam.adam_update(pd, g2, md, vd, 1, 1e-2)
+    assert np.array_equal(p, pd) and np.array_equal(m, md) and np.array_equal(v, vd)
+    assert list(np.nonzero(adam.touched_groups(np.r_[np.zeros(17), 1.0, np.zeros(3)]))[0]) == [16, 17, 18, 19, 20]
+
+
 # ---------------------------------------------------- P13/P14/P18 sampler
 def test_trilinear_identity_midpoint_linear():
     vol = np.random.default_rng(8).random((2, 2, 2)).astype(np.float32)
