@@ -36,7 +36,8 @@ def launches(path, out, cmd):
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
-    ours = {k: v for k, v in agg.items() if k.startswith('inr::')}
+    # (names may carry the inr:: namespace or not, depending on the ncu name base)
+    ours = {k.replace('inr::', ''): v for k, v in agg.items() if k.startswith('inr::') or '_kernel' in k}
     # one launch of each per fp16 fit step; prep_image also serves the decodes, so the
     # share uses per-launch averages: avg(kernel) / sum of the step kernels' averages
     stepk = ('step_begin', 'sample_kernel', 'encode_fwd', 'prep_image', 'mlp_fit', 'encode_bwd', 'adam')
