@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -495,8 +496,11 @@ extern "C" inr_status inr_reset_optimizer(inr_model* m) {
   return INR_OK;
 }
 
+static void purge_graphs(const inr_model* m);
+
 extern "C" inr_status inr_destroy(inr_model* m) {
   if (!m) return INR_OK;
+  purge_graphs(m);   // cached fit graphs holding this model's pointers
   cudaSetDevice(m->device);
   if ((m->host_resident || m->h16) && m->params) cudaFree(m->params);
   if (m->mesh) cudaFree(m->mesh);
@@ -647,6 +651,52 @@ static void keep_pool(int device) {
   done[device] = true;
 }
 
+// One-step CUDA graphs of recent fit calls.  A graph's kernels read everything by
+// value from their launch parameters (GroupArgs, FitScalars, AdamScalars, the
+// workspace pointers), so a later call whose parameter bytes are identical replays
+// the cached graph instead of capturing and instantiating a new one (the host
+// cost of a capture is ~1 ms, a step ~1.3 ms).  Each entry owns its workspace.
+// Entries are dropped by inr_destroy (a model's memory may be reused).
+struct FitGraph {
+  std::vector<unsigned char> key;
+  cudaGraphExec_t exec = nullptr;
+  void* ws = nullptr;
+  int device = -1;
+  unsigned long long last_use = 0;
+  int users = 0;                  // fit calls replaying it right now (never evicted then)
+};
+static std::mutex g_graph_mu;
+static std::list<FitGraph> g_graphs;
+static unsigned long long g_graph_clock = 0;
+constexpr size_t kGraphCache = 4;
+
+static void free_graph(FitGraph& f) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(f.device);
+  if (f.exec) cudaGraphExecDestroy(f.exec);
+  if (f.ws) cudaFree(f.ws);
+  cudaSetDevice(cur);
+  f.exec = nullptr;
+  f.ws = nullptr;
+}
+
+// Drop the cached graphs whose launch parameters hold this model's parameter pointer.
+static void purge_graphs(const inr_model* m) {
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  const void* p = m->params;
+  for (auto it = g_graphs.begin(); it != g_graphs.end();) {
+    bool hit = false;
+    for (size_t i = 0; !hit && i + sizeof p <= it->key.size(); ++i) hit = !memcmp(&it->key[i], &p, sizeof p);
+    if (hit && it->users == 0) {
+      free_graph(*it);
+      it = g_graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 static inr_status fit_impl(inr_model* const* models, const inr_view* views, int32_t nmodels, int32_t steps,
                            int32_t batch, const inr_fit_opts* opts, inr_fit_report* out, cudaStream_t st) {
   if (!models || !views || nmodels < 1) return fail(INR_ERR_INVALID_ARG, "models/views missing");
@@ -684,11 +734,13 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   if (tc && !tc_supported(m0->net)) return fail(INR_ERR_UNSUPPORTED, "configuration not supported by the tcgen05 MLP");
 
   FitScalars fs;
+  memset(&fs, 0, sizeof fs);   // (the parameter bytes key the graph cache)
   fs.B_u = batch;
   fs.B_b = opts->boundary_batch;
   fs.lambda = (float)opts->lambda;
   fs.det = m0->cfg.reduction == INR_REDUCE_DETERMINISTIC;
   AdamScalars as;
+  memset(&as, 0, sizeof as);
   as.lr0 = opts->lr0;
   as.lr_decay = opts->lr_decay;
   as.lr_step = opts->lr_step;
@@ -741,15 +793,54 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     }
   };
   build_groups();
-  // fp16 path: level-major pipeline with a per-call workspace (stream-ordered allocation)
-  void* ws_mem = nullptr;
-  LmWorkspace ws{};
-  if (tc) {
-    const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
-    const int per = std::min(nmodels, kMaxGroup);
-    CK(cudaMallocAsync(&ws_mem, lm_workspace_bytes(m0->net, per, Bs), st));
-    ws = lm_workspace(ws_mem, m0->net, per, Bs);
+  const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
+  const int launches_per_step = (tc ? 6 : 3) * nchunks;   // (graphs only without probing: fixed groups)
+  // CUDA graphs (launch-gap free): without probing, one step is captured once and
+  // replayed per step, and the instantiated graph is cached across calls (above);
+  // while profiling, the whole loop (with its event records) is captured once, so
+  // per-kernel timings come from the same graph execution.
+  const bool graphs = st != nullptr && !probing;
+  const bool whole = graphs && g_prof_on && steps >= 2;
+  const bool cached = graphs && !whole;
+  const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
+  const int per = std::min(nmodels, kMaxGroup);
+  const size_t ws_bytes = tc ? lm_workspace_bytes(m0->net, per, Bs) : 0;
+  std::vector<unsigned char> key;
+  if (cached) {
+    auto put = [&](const void* p, size_t n) {
+      const unsigned char* b = (const unsigned char*)p;
+      key.insert(key.end(), b, b + n);
+    };
+    int hdr[5] = {m0->device, (int)tc, Bs, nchunks, (int)ws_bytes};
+    put(hdr, sizeof hdr);
+    put(&fs, sizeof fs);
+    put(&as, sizeof as);
+    for (int c = 0; c < nchunks; ++c) put(&groups[c], sizeof(GroupArgs));
   }
+  // fp16 path: level-major pipeline with a workspace (per call, stream-ordered; or the
+  // cached graph's own)
+  void* ws_mem = nullptr;        // per-call workspace (freed at the end of the call)
+  void* ws_base = nullptr;
+  LmWorkspace ws{};
+  cudaGraphExec_t exec = nullptr;
+  FitGraph* entry = nullptr;
+  std::unique_lock<std::mutex> glock(g_graph_mu, std::defer_lock);
+  if (cached) {
+    glock.lock();
+    for (auto& f : g_graphs)
+      if (f.device == m0->device && f.key == key) { entry = &f; break; }
+    if (entry) {
+      exec = entry->exec;
+      ws_base = entry->ws;
+      entry->last_use = ++g_graph_clock;
+      ++entry->users;
+    }
+  }
+  if (tc && !ws_base) {
+    if (cached) CK(cudaMalloc(&ws_base, ws_bytes));
+    else { CK(cudaMallocAsync(&ws_mem, ws_bytes, st)); ws_base = ws_mem; }
+  }
+  if (tc) ws = lm_workspace(ws_base, m0->net, per, Bs);
   auto enqueue_step = [&](cudaStream_t s) {
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
@@ -772,26 +863,47 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     void*& p; cudaStream_t s;
     ~WsFree() { if (p) cudaFreeAsync(p, s); }
   } ws_free{ws_mem, st};
-  const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = (tc ? 6 : 3) * nchunks;   // (graphs only without probing: fixed groups)
-  // CUDA graphs (launch-gap free): without probing, capture one step and replay it
-  // per step; while profiling, capture the whole loop (with its event records)
-  // once, so per-kernel timings come from the same graph execution.
-  cudaGraphExec_t exec = nullptr;
-  const bool graphs = st != nullptr && !probing && steps >= 2;
-  const bool whole = graphs && g_prof_on;
-  if (graphs) {
+  if (graphs && !exec) {
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     long long before = g_launches.load();
     for (int s = 0; s < (whole ? steps : 1); ++s) enqueue_step(st);
     g_launches.store(before);  // captured launches are counted per replay below
     cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamEndCapture"); }
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaGraphInstantiate"); }
+    if (cached) {   // insert, evicting the least recently used idle entry beyond kGraphCache
+      if (g_graphs.size() >= kGraphCache) {
+        auto lru = g_graphs.end();
+        for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+          if (it->users == 0 && (lru == g_graphs.end() || it->last_use < lru->last_use)) lru = it;
+        if (lru != g_graphs.end()) {
+          free_graph(*lru);
+          g_graphs.erase(lru);
+        }
+      }
+      FitGraph f;
+      f.key = key;
+      f.exec = exec;
+      f.ws = ws_base;
+      f.device = m0->device;
+      f.last_use = ++g_graph_clock;
+      f.users = 1;
+      g_graphs.push_back(std::move(f));
+      entry = &g_graphs.back();
+    }
   }
+  if (glock.owns_lock()) glock.unlock();
+  struct Release {   // the entry may be evicted again once this call is done with it
+    FitGraph*& e;
+    ~Release() {
+      if (!e) return;
+      std::lock_guard<std::mutex> lock(g_graph_mu);
+      --e->users;
+    }
+  } release{entry};
   int taken = 0;
   std::vector<double> psnr(nmodels, 0.0);
   std::vector<int> reached(nmodels, 0), steps_of(nmodels, -1);
@@ -799,7 +911,10 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     if (exec) {
       if (whole && s > 0) { taken = s + 1; continue; }
       cudaError_t e = cudaGraphLaunch(exec, st);
-      if (e != cudaSuccess) { cudaGraphExecDestroy(exec); return cuda_fail(e, "cudaGraphLaunch"); }
+      if (e != cudaSuccess) {
+        if (!cached) cudaGraphExecDestroy(exec);
+        return cuda_fail(e, "cudaGraphLaunch");
+      }
       count_launch((long long)launches_per_step * (whole ? steps : 1));
     } else {
       enqueue_step(st);
@@ -830,7 +945,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       }
     }
   }
-  if (exec) cudaGraphExecDestroy(exec);
+  if (exec && !cached) cudaGraphExecDestroy(exec);
   for (int i = 0; i < nmodels; ++i) {
     if (steps_of[i] < 0) steps_of[i] = taken;
     models[i]->steps += steps_of[i];

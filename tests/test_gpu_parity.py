@@ -459,6 +459,38 @@ def test_gradients_linear_regime_lambda(lam, prec):
     inr.inr_destroy(m)
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+def test_cached_fit_graphs_replay_bitwise(prec):
+    """inr_fit caches each call's one-step CUDA graph (keyed by its launch
+    parameter bytes) and replays it in later identical calls: 1 + 2 + 3 steps in
+    three calls, with another model's calls in between (another cache entry),
+    end bitwise where one 6-step call ends (deterministic mode); a destroyed
+    model's entries go, and a model created afterwards fits like a fresh one."""
+    vol = synth.g2_energy(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (16, 16, 16))[2]
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 128
+    a = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    b = make_gpu_model(blk, 4, reduction=1, precision=prec, **CFG1)
+    for n in (1, 2, 3):
+        inr.inr_fit(a, whole_view(vt), n, 1024, go, stream())
+        inr.inr_fit(b, whole_view(vt), n, 1024, go, stream())
+    ref = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    inr.inr_fit(ref, whole_view(vt), 6, 1024, go, stream())
+    assert inr.inr_steps(a) == 6 and np.array_equal(get_params(a), get_params(ref))
+    inr.inr_destroy(a)
+    inr.inr_destroy(ref)
+    c = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    d = make_gpu_model(blk, 3, reduction=1, precision=prec, **CFG1)
+    inr.inr_fit(c, whole_view(vt), 2, 1024, go, stream())
+    inr.inr_fit(c, whole_view(vt), 2, 1024, go, stream())
+    inr.inr_fit(d, whole_view(vt), 4, 1024, go, stream())
+    assert np.array_equal(get_params(c), get_params(d))
+    for m in (b, c, d):
+        inr.inr_destroy(m)
+
+
 def test_decode_grid_and_query_vs_oracle():
     vol = synth.g1_analytic(32).numpy()
     blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
