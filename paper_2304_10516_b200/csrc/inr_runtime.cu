@@ -794,7 +794,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   };
   build_groups();
   const bool probing = out && opts->target_psnr > 0.0 && opts->check_interval > 0;
-  const int launches_per_step = (tc ? 6 : 3) * nchunks;   // (graphs only without probing: fixed groups)
+  const int launches_per_step = (tc ? 5 : 3) * nchunks;   // (graphs only without probing: fixed groups)
   // CUDA graphs (launch-gap free): without probing, one step is captured once and
   // replayed per step, and the instantiated graph is cached across calls (above);
   // while profiling, the whole loop (with its event records) is captured once, so
@@ -845,8 +845,8 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
       if (tc) {
-        // (the gradient is zeroed inside encode_fwd; step_begin only advances the step)
-        { ProfScope p(PK_STEP_BEGIN, s); launch_step_begin(g, g.nmodels, m0->net.nparams, s); }
+        // (encode_fwd zeroes the gradient and draws the step's samples; prep_image then
+        // advances the step counters: no separate step_begin launch)
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
         { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.targets, ws.dfeat, ws.Bs, s); }

@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, Fit
     // the sample is drawn here (Philox, R8) for every level; level 0's CTAs also
     // store it with its trilinear target(s) for the MLP and the scatter kernels
     float x[3];
-    draw_sample(md, i, fs.B_u, (uint32_t)*md.step_cur, x);
+    // the step being executed: step_total, which prep_image_kernel advances after this kernel
+    draw_sample(md, i, fs.B_u, (uint32_t)*md.step_total, x);
     if (l == 0) {
       if (g.net.D == 1) {
         float t[1];
