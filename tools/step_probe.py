@@ -39,8 +39,7 @@ span = inr.inr_profile_span()
 prof = {k: inr.inr_profile_read(k) for k in ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "adam")}
 inr.inr_profile_enable(0)
 rep = d.fit(vol, 1, 65536, o, st, report=True)
-env = {k: os.environ.get(k) for k in ("INR_SPAN_MB", "INR_BWD_CHUNK", "INR_ADAM_CTAS") if os.environ.get(k)}
-print(json.dumps({"env": env, "ms_per_step_median": ts[len(ts) // 2], "ms_per_step_all": ts,
+print(json.dumps({"lib": inr.LIB_PATH, "ms_per_step_median": ts[len(ts) // 2], "ms_per_step_all": ts,
                   "coords_per_s": 8 * 81920 / (ts[len(ts) // 2] / 1e3),
                   "profiled_span_ms_per_step": span / K,
                   "per_step_ms": {k: v[0] / K for k, v in prof.items()},
