@@ -1,7 +1,7 @@
-"""cfg2 fit-step time on the production path (no profiling: one-step CUDA graph
-replayed per step), CUDA events around K steps, median of R repeats; then one
-profiled K-step run for per-kernel-class device time.  Knobs via env
-(INR_SPAN_MB, INR_BWD_CHUNK, INR_ADAM_CTAS) are read by libinr at first use.
+"""cfg2 fit-step time on the production path (no profiling: the cached one-step
+CUDA graph replayed per step), CUDA events around K steps, median of R repeats;
+then one profiled K-step run for per-kernel-class device time.  For A/B runs
+of two builds in one gpurun call, point INR_LIB_PATH at each libinr.so.
 
   python tools/step_probe.py [K] [R]
 """
