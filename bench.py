@@ -541,6 +541,23 @@ def run_ours(args):
               "kernel": "decode_grid: " + ("tcgen05 fp16 MLP, 8x4x4 bricks with staged coarse levels, R19 vertex "
                                            "elision; median of 5" if prec else "fp32 CUDA-core MLP; median of 5"),
               "queries_per_s": nq * world / (q_ms / 1e3), "queries": nq * world, "query_ms": q_ms}
+    try:   # the grid decode against the measured L2 gather rate (sectors per block from the ncu capture)
+        sec = None
+        for ln in open(os.path.join(ROOT, "profiles", "r2_ncu_decode.txt")):
+            if ln.strip().startswith("lts__t_sectors_srcunit_tex_op_read.sum"):
+                sec = float(ln.split()[1])
+        with open(os.path.join(ROOT, "profiles", "r1_l2_peaks.json")) as f:
+            gpk = {(r["op"], r["buffer_MB"]): r["per_s"] for r in json.load(f)["results"]}[("gather_8B", 64)]
+        if sec and prec:
+            rate = sec * len(d.models) / (dec_ms / 1e3)
+            decode["roofline"] = {"bound": "l2 random gather (R19 vertex gathers + staged brick boxes)",
+                                  "l2_sectors_per_block": sec, "achieved_sectors_per_s": rate,
+                                  "peak_accesses_per_s": gpk, "frac": rate / gpk,
+                                  "source": "profiles/r2_ncu_decode.txt (one 128^3 block) and r1_l2_peaks.json",
+                                  "note": "issue / latency bound (IPC ~2.6, 65% of issue slots; tensor pipe 7%), "
+                                          "not gather bound: see DESIGN.md §5"}
+    except (OSError, KeyError, ValueError, StopIteration):
+        pass
     if world > 1:   # a18: decoded slabs -> rank 0 (NCCL gather over NVLink), reported separately
         full = d.gather(out, 0)              # warm (NCCL communicator set-up)
         del full
