@@ -865,7 +865,10 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   } ws_free{ws_mem, st};
   if (graphs && !exec) {
     cudaGraph_t graph;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    {
+      cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamBeginCapture"); }
+    }
     long long before = g_launches.load();
     for (int s = 0; s < (whole ? steps : 1); ++s) enqueue_step(st);
     g_launches.store(before);  // captured launches are counted per replay below
