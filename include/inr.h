@@ -220,7 +220,13 @@ INR_API inr_status inr_fit(inr_model* m, const inr_view* block_values, int32_t s
  * if non-NULL, is an array of nmodels reports.  With PSNR-target stopping each
  * model leaves the group at the first check where it reaches the target, so it
  * ends exactly as if fitted alone (report.steps_taken per model) while the
- * others continue. */
+ * others continue.
+ * Execution (both calls): on a non-NULL stream and without PSNR-target stopping
+ * one step is captured as a CUDA graph and replayed per step; the instantiated
+ * graph and its workspace are cached (the last 4 distinct argument sets, keyed by
+ * every value the step's kernels read) so later calls with the same models,
+ * views and options replay it without a new capture; inr_destroy of any of the
+ * models releases the entry. */
 INR_API inr_status inr_fit_group(inr_model* const* models, const inr_view* views, int32_t nmodels,
                          int32_t steps, int32_t batch, const inr_fit_opts* opts,
                          inr_fit_report* out, cudaStream_t stream);
