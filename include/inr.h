@@ -244,7 +244,9 @@ INR_API inr_status inr_fit_losses(inr_model* const* models, int32_t nmodels, dou
  * v = Phi(x) (vmax - vmin) + vmin (per channel, channels interleaved).  A query p goes to the block
  * min(max(floor(p/n), 0), B-1) per axis and x = fl32(fl32(p - o)/n) [R5];
  * inr_decode uses the one model, inr_decode_group routes among `nmodels`
- * models (a point whose block is not among them gets NaN).  strict != 0
+ * models (a point whose block is not among them gets NaN; any number of models,
+ * decoded in routed passes of <= 64 models; at most 4096 blocks in the volume,
+ * else INR_ERR_UNSUPPORTED).  strict != 0
  * reports INR_ERR_DOMAIN after the fact if any coordinate lies outside
  * [0, N-1]^3 (values are still written, clamped); strict synchronizes. */
 INR_API inr_status inr_decode(const inr_model* m, const float* xyz, int64_t q, float* out, int32_t strict,

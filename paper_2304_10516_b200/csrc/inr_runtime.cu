@@ -1056,15 +1056,12 @@ extern "C" inr_status inr_decode_grid(const inr_model* m, const int32_t res[3], 
   return inr_decode_grid_part(m, res, nullptr, out, out_stride, ref, sse_dev, st);
 }
 
-static inr_status decode_group_impl(const inr_model* const* models, int32_t nmodels, const float* xyz, int64_t q,
-                                    float* out, int32_t strict, cudaStream_t st) {
-  if (!models || nmodels < 1 || (q > 0 && (!xyz || !out))) return fail(INR_ERR_INVALID_ARG, "NULL argument");
-  if (q < 0) return fail(INR_ERR_INVALID_ARG, "q must be >= 0");
-  if (nmodels > kMaxGroup) return fail(INR_ERR_UNSUPPORTED, "at most %d models per decode group", kMaxGroup);
+// One chunk of <= kMaxGroup models of a decode group: queries routed to blocks of
+// the chunk are decoded, those of the group's other chunks (slot -2) are left
+// untouched, those of blocks no model holds get NaN.
+static inr_status decode_chunk(const inr_model* const* models, int32_t nmodels, int32_t c0, int32_t c1,
+                               const float* xyz, int64_t q, float* out, int* dflag, cudaStream_t st) {
   const inr_model* m0 = models[0];
-  if (!m0) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
-  CK(cudaSetDevice(m0->device));
-  keep_pool(m0->device);
   QueryArgs* qa = new QueryArgs();
   memset(qa, 0, sizeof *qa);
   qa->net = m0->net;
@@ -1089,29 +1086,29 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
         delete qa;
         return fail(INR_ERR_INVALID_ARG, "decode group models must tile one volume");
       }
+    if (m->block_id >= (uint32_t)nb) { delete qa; return fail(INR_ERR_INVALID_ARG, "block id outside the volume"); }
+    if (i < c0 || i >= c1) {
+      qa->slot_of_block[m->block_id] = -2;
+      continue;
+    }
     inr_status s = ensure_device_params(m, st);
     if (s) { delete qa; return s; }
-    qa->md[i] = model_dev(m);
-    qa->slot_of_block[m->block_id] = (int16_t)i;
+    qa->md[i - c0] = model_dev(m);
+    qa->slot_of_block[m->block_id] = (int16_t)(i - c0);
   }
-  int* dflag = nullptr;
-  if (strict) {
-    cudaError_t e = cudaMallocAsync((void**)&dflag, sizeof(int), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int), st);
-    if (e != cudaSuccess) { delete qa; return cuda_fail(e, "strict flag"); }
-  }
-  qa->nmodels = nmodels;
+  const int nm = c1 - c0;
+  qa->nmodels = nm;
   if (q > 0 && m0->cfg.precision == INR_PREC_FP16_MLP) {
     // tensor-core path: bucket the queries by block, then 128-query tiles of one block each
     void* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, query_workspace_bytes(q, nmodels), st);
+    cudaError_t e = cudaMallocAsync(&ws, query_workspace_bytes(q, nm), st);
     if (e != cudaSuccess) { delete qa; return cuda_fail(e, "query workspace"); }
     QueryBuckets qb;
     launch_query_buckets(*qa, xyz, q, out, dflag, ws, qb, st);
     GroupArgs* g = new GroupArgs();
     g->net = qa->net;
-    g->nmodels = nmodels;
-    for (int i = 0; i < nmodels; ++i) g->md[i] = qa->md[i];
+    g->nmodels = nm;
+    for (int i = 0; i < nm; ++i) g->md[i] = qa->md[i];
     { ProfScope p(PK_DECODE_QUERY, st); launch_decode_query_tc(*g, xyz, q, out, qb, st); }
     delete g;
     cudaFreeAsync(ws, st);
@@ -1120,6 +1117,28 @@ static inr_status decode_group_impl(const inr_model* const* models, int32_t nmod
     launch_decode_query_simt(*qa, xyz, q, out, dflag, st);
   }
   delete qa;
+  return INR_OK;
+}
+
+static inr_status decode_group_impl(const inr_model* const* models, int32_t nmodels, const float* xyz, int64_t q,
+                                    float* out, int32_t strict, cudaStream_t st) {
+  if (!models || nmodels < 1 || (q > 0 && (!xyz || !out))) return fail(INR_ERR_INVALID_ARG, "NULL argument");
+  if (q < 0) return fail(INR_ERR_INVALID_ARG, "q must be >= 0");
+  const inr_model* m0 = models[0];
+  if (!m0) return fail(INR_ERR_INVALID_ARG, "model 0 is NULL");
+  CK(cudaSetDevice(m0->device));
+  keep_pool(m0->device);
+  int* dflag = nullptr;
+  if (strict) {
+    cudaError_t e = cudaMallocAsync((void**)&dflag, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dflag, 0, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "strict flag");
+  }
+  // groups of more than kMaxGroup models: one routed pass per chunk of models
+  for (int c0 = 0; c0 < nmodels; c0 += kMaxGroup) {
+    inr_status s = decode_chunk(models, nmodels, c0, std::min(nmodels, c0 + kMaxGroup), xyz, q, out, dflag, st);
+    if (s) { if (dflag) cudaFreeAsync(dflag, st); return s; }
+  }
   CK_LAUNCH("decode_query");
   if (strict) {
     int h = 0;

@@ -251,8 +251,10 @@ __global__ void route_kernel(QueryArgs qa, const float* __restrict__ xyz, long l
     const int bid = (bc[2] * qa.B[1] + bc[1]) * qa.B[0] + bc[0];
     const int slot = bid < qa.nblocks ? qa.slot_of_block[bid] : -1;
     slot_of[j] = slot;
+    // slot -1: no model has this block (NaN); -2: another chunk of the group decodes it
     if (slot >= 0) atomicAdd(cnt + slot, 1);
-    else out[j] = __int_as_float(0x7fc00000);
+    else if (slot == -1)
+      for (int c = 0; c < qa.net.D; ++c) out[j * qa.net.D + c] = __int_as_float(0x7fc00000);
     if (outside && dflag) atomicOr(dflag, 1);
   }
   __syncthreads();

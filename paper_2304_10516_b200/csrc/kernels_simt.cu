@@ -363,10 +363,11 @@ __global__ void __launch_bounds__(kTile) decode_query_simt_kernel(QueryArgs qa, 
   encode_to_smem<F>(qa.net, md.params, x, smem, t);
   float y[kMaxD];
   mlp_forward_simt(qa.net, md.params, smem, t, y);
-  if (valid) {
+  if (valid) {   // (slot -2: another chunk of the group decodes this query)
     const int D = qa.net.D;
-    for (int c = 0; c < D; ++c)
-      out[j * D + c] = slot < 0 ? __int_as_float(0x7fc00000) : fmaf(y[c], md.vrange[c], md.vmin[c]);
+    if (slot != -2)
+      for (int c = 0; c < D; ++c)
+        out[j * D + c] = slot < 0 ? __int_as_float(0x7fc00000) : fmaf(y[c], md.vrange[c], md.vmin[c]);
     if (outside && domain_flag) atomicOr(domain_flag, 1);
   }
 }

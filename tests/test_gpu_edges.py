@@ -250,3 +250,43 @@ def test_block_psnrs_pool_to_the_global_psnr():
     assert abs(-10 * np.log10(pooled) - d.psnr(float(sse.item()), 40 ** 3)) < 1e-6
     assert len(bp) == 27 and min(bp.values()) <= -10 * np.log10(pooled) + 1e-9
     d.close()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_groups_larger_than_one_launch(prec):
+    """72 blocks (6 x 6 x 2 of 8^3) exceed one fused launch's 64 models: the fit
+    runs as two chunks and the query decode routes over all 72.  Each block ends
+    bitwise as if fitted alone (deterministic mode), chunk boundary included, and
+    the group query decode equals every block's own grid decode at the nodes."""
+    vol = synth.g2_energy(48).numpy()[:16]                  # 48 x 48 x 16 nodes (z, y, x)
+    dims = (48, 48, 16)
+    blocks = sampler.decompose(dims, (8, 8, 8))
+    assert len(blocks) == 72
+    net = dict(levels=8, features=2, log2_table_size=10, mlp_hidden_layers=1)
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 32
+    ms = [make_gpu_model(b, 4, precision=prec, reduction=1, **net) for b in blocks]
+    reps = inr.inr_fit_group(ms, [whole_view(vt)] * 72, 3, 256, go, stream())
+    assert all(r.steps_taken == 3 for r in reps)
+    from gpu_util import get_params
+    for k in (0, 63, 64, 71):
+        single = make_gpu_model(blocks[k], 4, precision=prec, reduction=1, **net)
+        inr.inr_fit(single, whole_view(vt), 3, 256, go, stream())
+        assert np.array_equal(get_params(single), get_params(ms[k])), k
+        inr.inr_destroy(single)
+    full = torch.empty((16, 48, 48), device="cuda")
+    for m, b in zip(ms, blocks):
+        o = b.origin
+        cnt = tuple(min(8, dims[d] - o[d]) for d in range(3))
+        inr.inr_decode_grid(m, (8, 8, 8), full[o[2]:, o[1]:, o[0]:].data_ptr(), (1, 48, 48 * 48), None, None,
+                            stream(), count=cnt)
+    z, y, x = np.meshgrid(np.arange(16), np.arange(48), np.arange(48), indexing="ij")
+    pts = np.stack([x.ravel(), y.ravel(), z.ravel()], 1).astype(np.float32)
+    pd = torch.from_numpy(pts).cuda()
+    q = torch.empty(pts.shape[0], device="cuda")
+    inr.inr_decode_group(ms, pd.data_ptr(), pts.shape[0], q.data_ptr(), 1, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(q, full.reshape(-1))
+    for m in ms:
+        inr.inr_destroy(m)

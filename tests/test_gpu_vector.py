@@ -108,6 +108,13 @@ def test_decode_vector_grid_and_query(prec, tol):
     inr.inr_decode_group(gms, pd.data_ptr(), pts.shape[0], q.data_ptr(), 1, stream())
     torch.cuda.synchronize()
     assert normwise(q.cpu().numpy(), o_decode.decode_query(oms, pts)) <= tol
+    # a group without block 0: its points get NaN in all three channels, the others are untouched
+    q2 = torch.full((pts.shape[0], 3), 7.0, device="cuda")
+    inr.inr_decode_group(gms[1:], pd.data_ptr(), pts.shape[0], q2.data_ptr(), 0, stream())
+    torch.cuda.synchronize()
+    in0 = np.all(np.minimum(np.floor(pts / 16), 1) == 0, axis=1)
+    q2n = q2.cpu().numpy()
+    assert in0.any() and np.isnan(q2n[in0]).all() and np.array_equal(q2n[~in0], q.cpu().numpy()[~in0])
     # SSE against the ground truth at the nodes, pooled over channels in normalized units
     full = torch.empty((32, 32, 32, 3), device="cuda")
     sse = torch.zeros(1, dtype=torch.float64, device="cuda")
