@@ -290,3 +290,39 @@ def test_groups_larger_than_one_launch(prec):
     assert torch.equal(q, full.reshape(-1))
     for m in ms:
         inr.inr_destroy(m)
+
+
+def test_concurrent_fits_from_two_host_threads():
+    """Distinct models are independent (inr.h): two host threads fitting their
+    own models on their own streams at the same time (ctypes releases the GIL;
+    both go through the fit-graph cache) end bitwise where sequential fits end
+    (deterministic mode)."""
+    import threading
+    vol = synth.g2_energy(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch = float(vol.min()), float(vol.max()), 64
+    net = dict(levels=8, features=2, log2_table_size=12, mlp_hidden_layers=2)
+    from gpu_util import get_params
+
+    def fit(ms, st, reps):
+        for _ in range(reps):
+            inr.inr_fit_group(ms, [whole_view(vt)] * len(ms), 3, 2048, go, st.cuda_stream, False)
+        st.synchronize()
+
+    a = [make_gpu_model(b, 9, precision=1, reduction=1, **net) for b in blocks[:4]]
+    b = [make_gpu_model(b, 9, precision=1, reduction=1, **net) for b in blocks[4:]]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    th = [threading.Thread(target=fit, args=(a, s1, 5)), threading.Thread(target=fit, args=(b, s2, 5))]
+    for t_ in th:
+        t_.start()
+    for t_ in th:
+        t_.join()
+    ref = [make_gpu_model(bl, 9, precision=1, reduction=1, **net) for bl in blocks]
+    fit(ref[:4], s1, 5)
+    fit(ref[4:], s1, 5)
+    for m, r in zip(a + b, ref):
+        assert np.array_equal(get_params(m), get_params(r))
+    for m in a + b + ref:
+        inr.inr_destroy(m)
