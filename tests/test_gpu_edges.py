@@ -326,3 +326,35 @@ def test_concurrent_fits_from_two_host_threads():
         assert np.array_equal(get_params(m), get_params(r))
     for m in a + b + ref:
         inr.inr_destroy(m)
+
+
+def test_legacy_default_stream_fit_and_snapshot_staging_on_two_streams():
+    """inr_fit on the legacy default stream (NULL: no CUDA graph) ends bitwise
+    where the same fit on a created stream (cached graph) ends; a host-resident
+    fp16 cache snapshot decoded first on one stream and at once on another gets
+    the same values on both (its staging completes before either decode reads it)."""
+    vol = synth.g1_analytic(32).numpy()
+    blk = sampler.decompose((32, 32, 32), (32, 32, 32))[0]
+    vt = gpu_volume(vol)
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax = float(vol.min()), float(vol.max())
+    from gpu_util import get_params
+    a = make_gpu_model(blk, 3, precision=1, reduction=1, **NET)
+    b = make_gpu_model(blk, 3, precision=1, reduction=1, **NET)
+    inr.inr_fit(a, whole_view(vt), 4, 1024, go, 0)
+    inr.inr_fit(b, whole_view(vt), 4, 1024, go, stream())
+    assert np.array_equal(get_params(a), get_params(b))
+    c = inr.cache_create(2, inr.CACHE_HOST_RESIDENT | inr.CACHE_FP16, 0)
+    inr.cache_insert(c, 1, [a], stream())
+    torch.cuda.synchronize()
+    _, snap = inr.cache_get(c, 0)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1 = torch.empty((32, 32, 32), device="cuda")
+    o2 = torch.empty((32, 32, 32), device="cuda")
+    inr.inr_decode_grid(snap[0], (32, 32, 32), o1.data_ptr(), None, None, None, s1.cuda_stream)
+    inr.inr_decode_grid(snap[0], (32, 32, 32), o2.data_ptr(), None, None, None, s2.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.isfinite(o1).all()
+    inr.cache_destroy(c)
+    inr.inr_destroy(a)
+    inr.inr_destroy(b)
