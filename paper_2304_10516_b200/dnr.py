@@ -78,6 +78,24 @@ def is_block_box(block_ids, global_dims, n):
     return len(set(block_ids)) == (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1)
 
 
+def _send(t, dst):
+    """Point-to-point send of a CUDA tensor: direct with NCCL; staged through host
+    memory with gloo (its CPU transport), e.g. several ranks sharing one GPU."""
+    if dist.get_backend() == "nccl":
+        dist.send(t, dst)
+    else:
+        dist.send(t.cpu(), dst)
+
+
+def _recv(t, src):
+    if dist.get_backend() == "nccl":
+        dist.recv(t, src)
+    else:
+        h = torch.empty(t.shape, dtype=t.dtype)
+        dist.recv(h, src)
+        t.copy_(h)
+
+
 def _dev():
     return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
 
@@ -334,6 +352,7 @@ class DNR:
                     owner = next(own for own in range(self.world) if b in partition_blocks(self.nblocks, self.world, own))
                     held[b], steps[b] = self._recv_block(b, src, owner, stream)
                 moved.append((b, src, dst))
+        self.last_moved = list(moved)
         # stolen blocks go home: the holder returns the final state to the owner
         home = {}
         for b, src, dst in moved:
@@ -347,31 +366,31 @@ class DNR:
                 e = held.pop(b)
                 self._send_state(e["model"], owner, stream)
                 done_b = done.pop(b)
-                dist.send(torch.tensor([done_b[0], int(done_b[1])], dtype=torch.int64, device=dev), owner)
+                _send(torch.tensor([done_b[0], int(done_b[1])], dtype=torch.int64, device=dev), owner)
                 inr.inr_destroy(e["model"])
             elif self.rank == owner:
                 m = self.models[self.block_ids.index(b)]
                 self._recv_state(m, holder, stream)
                 t = torch.empty(2, dtype=torch.int64, device=dev)
-                dist.recv(t, holder)
+                _recv(t, holder)
                 done[b] = (int(t[0]), bool(t[1]))
         return {b: done[b] for b in self.block_ids}
 
     def _send_state(self, m, dst, stream):
         buf = torch.empty(self.inr.inr_state_bytes(m), dtype=torch.uint8, device=torch.device("cuda", self.device))
         self.inr.inr_export_state(m, buf.data_ptr(), stream)
-        dist.send(buf, dst)
+        _send(buf, dst)
 
     def _recv_state(self, m, src, stream):
         buf = torch.empty(self.inr.inr_state_bytes(m), dtype=torch.uint8, device=torch.device("cuda", self.device))
-        dist.recv(buf, src)
+        _recv(buf, src)
         torch.cuda.current_stream().synchronize()
         self.inr.inr_import_state(m, buf.data_ptr(), stream)
 
     def _send_block(self, entry, b, dst, stream, nsteps):
         """State, steps taken in this fit and the block's node box of the volume to rank dst."""
         self._send_state(entry["model"], dst, stream)
-        dist.send(torch.tensor([nsteps], dtype=torch.int64, device=torch.device("cuda", self.device)), dst)
+        _send(torch.tensor([nsteps], dtype=torch.int64, device=torch.device("cuda", self.device)), dst)
         o, hi = self._box(b)
         if entry["vol"] is not None:
             box = entry["vol"]
@@ -379,7 +398,7 @@ class DNR:
             lv = self._local_volume_for_send
             box = lv[o[2] - self.lo[2]:hi[2] - self.lo[2] + 1, o[1] - self.lo[1]:hi[1] - self.lo[1] + 1,
                      o[0] - self.lo[0]:hi[0] - self.lo[0] + 1].contiguous()
-        dist.send(box, dst)
+        _send(box, dst)
         if entry["model"] not in self.models:        # a block this rank had stolen itself
             self.inr.inr_destroy(entry["model"])
 
@@ -388,11 +407,11 @@ class DNR:
         m = self.inr.inr_create(self.cfg, self.inr.make_block(o, self.n, self.global_dims), self.device)
         self._recv_state(m, src, stream)
         t = torch.empty(1, dtype=torch.int64, device=torch.device("cuda", self.device))
-        dist.recv(t, src)
+        _recv(t, src)
         dims = tuple(hi[d] - o[d] + 1 for d in range(3))
         shape = (dims[2], dims[1], dims[0]) + ((self.D,) if self.D > 1 else ())
         vol = torch.empty(shape, dtype=torch.float32, device=torch.device("cuda", self.device))
-        dist.recv(vol, src)
+        _recv(vol, src)
         torch.cuda.current_stream().synchronize()
         v = self.inr.make_view(vol.data_ptr(), o, dims, self._strides(dims[0], dims[1]), self.D)
         return dict(model=m, view=v, owner=owner, vol=vol), int(t.item())

@@ -88,7 +88,80 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, backend, tmp):
+CAM = dict(eye=(-40.0, 85.0, -60.0), look=(32.0, 30.0, 33.0), up=(0.0, 1.0, 0.0), fovy=40.0, width=56, height=44)
+TF_POINTS = [0.0, 0.3, 0.6, 1.0]
+TF_RGBA = [[0.0, 0.0, 1.0, 0.0], [0.0, 0.4, 1.0, 0.02], [0.2, 1.0, 0.3, 0.08], [1.0, 0.2, 0.0, 0.4]]
+
+
+def _decode_and_render(rank, world, vol_np):
+    """Fit (as _fit_and_decode), then the two consumers that cross ranks through
+    peer memory: decode_to_rank (every rank's decode kernels store into rank 0's
+    global volume) and the sort-last render (fragments stored into rank 0's
+    stack, composited there).  Returns (volume, image) on rank 0, Nones elsewhere."""
+    from paper_2304_10516_b200 import dnr, inr
+    cfg = inr.make_config(seed=5, precision=inr.INR_PREC_FP16_MLP, reduction=inr.INR_REDUCE_DETERMINISTIC, **NET)
+    d = dnr.DNR(GDIMS, BLOCK, cfg, rank, world, torch.cuda.current_device())
+    lo, hi = d.lo, d.hi
+    vol = torch.from_numpy(np.ascontiguousarray(vol_np[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1])).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    d.value_range(vol, st)
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = 512
+    d.fit(vol, STEPS, BATCH, opts, st, report=False)
+    target = d.peer_volume(0)
+    full = d.decode_to_rank(target, st)
+    full = full.cpu().numpy() if full is not None else None
+    cam = inr.make_camera(CAM["eye"], CAM["look"], CAM["up"], CAM["fovy"], CAM["width"], CAM["height"])
+    tf = inr.make_tf(TF_POINTS, TF_RGBA, d.vmin, d.vmax, 1.0)
+    # stop_alpha > 1: no early ray termination, so splitting the ray at the brick face
+    # changes nothing but the compositing's rounding (S:L486)
+    img = d.render(cam, tf, 0.5, background=(0.1, 0.1, 0.1), stop_alpha=2.0, stream=st)
+    img = img.cpu().numpy() if img is not None else None
+    d.close()
+    return full, img
+
+
+def _steal_volume():
+    """Rank 1's slab (z > 32) is a constant, which its blocks fit to the target
+    in the first round; rank 0's blocks hold the G2 field plus uniform noise of
+    60 % of the range (an error floor far below the 32 dB target, even on the
+    probe lattice's trilinearly smoothed samples), so they run
+    to max_steps: rank 1 goes idle and steals half of rank 0's unfinished blocks."""
+    v = _volume().copy()
+    lo, hi = float(v.min()), float(v.max())
+    noise = np.random.RandomState(3).uniform(-0.3, 0.3, v.shape).astype(np.float32) * (hi - lo)
+    v = np.clip(v + noise, lo, hi)
+    v[33:] = 0.5 * (lo + hi)
+    return v
+
+
+def _fit_to_target(rank, world, vol_np, steal):
+    """DNR.fit_to_target from fresh models; returns ({block: (steps, reached)},
+    {block: final parameters}, blocks that moved)."""
+    from paper_2304_10516_b200 import dnr, inr
+    cfg = inr.make_config(seed=9, precision=inr.INR_PREC_FP16_MLP, reduction=inr.INR_REDUCE_DETERMINISTIC, **NET)
+    d = dnr.DNR(GDIMS, BLOCK, cfg, rank, world, torch.cuda.current_device())
+    lo, hi = d.lo, d.hi
+    vol = torch.from_numpy(np.ascontiguousarray(vol_np[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1])).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    d.value_range(vol, st)
+    opts = inr.inr_fit_opts_default()
+    opts.boundary_batch = 512
+    res = d.fit_to_target(vol, 32.0, 600, BATCH, opts, check_interval=50, round_steps=100, steal=steal, stream=st)
+    torch.cuda.synchronize()
+    params = {}
+    for b, m in zip(d.block_ids, d.models):
+        p = np.empty(inr.inr_param_count(m), np.float32)
+        inr.inr_get_params(m, p)
+        params[b] = p
+    moved = list(getattr(d, "last_moved", []))
+    d.close()
+    return res, params, moved
+
+
+def _rank_main(rank, world, port, backend, tmp, mode="fit"):
+    import pickle
+
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dev = rank if backend == "nccl" else 0
@@ -97,27 +170,44 @@ def _rank_main(rank, world, port, backend, tmp):
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
     else:
         dist.init_process_group("gloo", rank=rank, world_size=world)
-    core, lo, n = _fit_and_decode(rank, world, _volume())
-    np.save(os.path.join(tmp, f"core{rank}.npy"), core)
-    np.save(os.path.join(tmp, f"meta{rank}.npy"), np.array(list(lo) + [n], np.int64))
+    if mode == "fit":
+        core, lo, n = _fit_and_decode(rank, world, _volume())
+        np.save(os.path.join(tmp, f"core{rank}.npy"), core)
+        np.save(os.path.join(tmp, f"meta{rank}.npy"), np.array(list(lo) + [n], np.int64))
+    elif mode == "consumers":
+        full, img = _decode_and_render(rank, world, _volume())
+        if rank == 0:
+            np.save(os.path.join(tmp, "full.npy"), full)
+            np.save(os.path.join(tmp, "img.npy"), img)
+        else:
+            assert full is None and img is None
+    else:
+        out = _fit_to_target(rank, world, _steal_volume(), steal=True)
+        with open(os.path.join(tmp, f"steal{rank}.pkl"), "wb") as f:
+            pickle.dump(out, f)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _spawn(mode, tmp):
+    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, backend, tmp, mode)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(600)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    return backend
 
 
 def test_two_ranks_decode_equals_one_rank_and_fit_has_no_collectives():
     vol = _volume()
     ref, lo1, n1 = _fit_and_decode(0, 1, vol)           # one process, every block
     assert ref.shape == (64, 64, 64) and tuple(lo1) == (0, 0, 0) and n1 == 0
-    backend = "nccl" if torch.cuda.device_count() >= 2 else "gloo"
     with tempfile.TemporaryDirectory() as tmp:
-        ctx = mp.get_context("spawn")
-        port = _free_port()
-        ps = [ctx.Process(target=_rank_main, args=(r, 2, port, backend, tmp)) for r in range(2)]
-        for p in ps:
-            p.start()
-        for p in ps:
-            p.join(600)
-        assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+        backend = _spawn("fit", tmp)
         full = np.full((64, 64, 64), np.nan, np.float32)
         for r in range(2):
             core = np.load(os.path.join(tmp, f"core{r}.npy"))
@@ -128,3 +218,49 @@ def test_two_ranks_decode_equals_one_rank_and_fit_has_no_collectives():
     print("backend", backend, "max |2-rank - 1-rank|", float(np.nanmax(np.abs(full - ref))))
     assert not np.isnan(full).any()
     assert np.array_equal(full, ref)                     # bitwise (deterministic reduction)
+
+
+def test_peer_decode_and_sort_last_render_across_ranks():
+    """decode_to_rank: both ranks' decode kernels store into rank 0's volume
+    through peer memory (CUDA IPC; cudaIpc on one device when the box has one
+    GPU) -- bitwise the one-process decode.  render: each rank ray-marches its
+    brick and stores its fragments into rank 0's stack, rank 0 depth-composites
+     -- the one-process image up to the compositing's rounding."""
+    vol = _volume()
+    ref_full, ref_img = _decode_and_render(0, 1, vol)
+    assert ref_img[:, 3].max() > 0.3                     # a non-trivial image
+    with tempfile.TemporaryDirectory() as tmp:
+        backend = _spawn("consumers", tmp)
+        full = np.load(os.path.join(tmp, "full.npy"))
+        img = np.load(os.path.join(tmp, "img.npy"))
+    err = float(np.max(np.abs(img - ref_img)))
+    print("backend", backend, "render max |2-rank - 1-rank|", err)
+    assert np.array_equal(full, ref_full)
+    assert err <= 2e-6                                   # test_gpu_render: the split costs ~1 ulp
+
+
+def test_block_stealing_gives_the_unstolen_result():
+    """fit_to_target with block stealing (NEXT-4): rank 1 finishes its blocks,
+    steals two of rank 0's, fits them on its own device from the transferred
+    state + node box, and returns the final state.  Blocks are independent and
+    the deterministic reduction does not depend on grouping, so every block's
+    parameters and step count are bitwise those of one process fitting all eight
+    with no stealing."""
+    import pickle
+    vol = _steal_volume()
+    ref_res, ref_params, ref_moved = _fit_to_target(0, 1, vol, steal=False)
+    assert ref_moved == []
+    with tempfile.TemporaryDirectory() as tmp:
+        backend = _spawn("steal", tmp)
+        outs = []
+        for r in range(2):
+            with open(os.path.join(tmp, f"steal{r}.pkl"), "rb") as f:
+                outs.append(pickle.load(f))
+    moved = outs[0][2]
+    print("backend", backend, "moved", moved, "steps", {b: s for o in outs for b, s in o[0].items()})
+    assert moved and outs[1][2] == moved and all(src == 0 and dst == 1 for _, src, dst in moved)
+    res = {**outs[0][0], **outs[1][0]}
+    params = {**outs[0][1], **outs[1][1]}
+    assert res == ref_res
+    for b in range(8):
+        assert np.array_equal(params[b], ref_params[b]), b
