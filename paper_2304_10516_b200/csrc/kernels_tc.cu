@@ -248,14 +248,16 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
 #pragma unroll
       for (int c = 0; c < kFitCW; c += 16) tmem_ld16(tmem + lane_base + cb + c, z + c);
       tmem_wait_ld();
-      const float cap = valid ? INFINITY : 0.f;   // padding rows: h = 0
+      // padding rows (i >= total) need no clamp: their h_0 rows are zeros and the ones
+      // group (encode_fwd), so every activation stays finite, and their dy = 0 makes
+      // every dz row 0, so they add nothing to dW, db or dfeat
 #pragma unroll
       for (int n = 0; n < kFitCW; n += 4) {
         const float4 b4 = *reinterpret_cast<const float4*>(bias + k * 64 + cb + n);
-        z[n] = fmaxf(fminf(z[n] + b4.x, cap), 0.f);
-        z[n + 1] = fmaxf(fminf(z[n + 1] + b4.y, cap), 0.f);
-        z[n + 2] = fmaxf(fminf(z[n + 2] + b4.z, cap), 0.f);
-        z[n + 3] = fmaxf(fminf(z[n + 3] + b4.w, cap), 0.f);
+        z[n] = fmaxf(z[n] + b4.x, 0.f);
+        z[n + 1] = fmaxf(z[n + 1] + b4.y, 0.f);
+        z[n + 2] = fmaxf(z[n + 2] + b4.z, 0.f);
+        z[n + 3] = fmaxf(z[n + 3] + b4.w, 0.f);
       }
       if (k + 1 < H) {
 #pragma unroll
@@ -398,10 +400,12 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
           }
         } else if (valid) {
           // dfeat, unscaled, level-major (coalesced across the tile)
+          float* const o0 = dfeatm + ((size_t)(q * (kFitCW / F)) * Bs + i) * F;
+          const size_t lstride = (size_t)Bs * F;
 #pragma unroll
           for (int c = 0; c < kFitCW; c += F) {
             if (cb + c < net.LF) {
-              float* o = dfeatm + ((size_t)((cb + c) / F) * Bs + i) * F;
+              float* o = o0 + (size_t)(c / F) * lstride;
               if constexpr (F == 1) { o[0] = dh[c] * inv_scale; }
               else if constexpr (F == 2) { *reinterpret_cast<float2*>(o) = make_float2(dh[c] * inv_scale, dh[c + 1] * inv_scale); }
               else {
@@ -617,6 +621,7 @@ struct FwdArgs {
   int nst;                            // MODE 1: levels [0, nst) are staged per brick in shared memory
   int st_off[kMaxLevels + 1];         //   float offset of level l's vertex box in the stage area
   int na;                             // MODE 1: levels [na, L) are vertex-aligned (one entry per point, R19)
+  float rinv[3];                      //   1 / R_d when R_d is a power of two (x_j = j / R_d exactly), else 0
 };
 
 // MODE 1 brick staging (grid decode): the levels coarser than the
@@ -646,15 +651,17 @@ template <int F>
 __device__ __forceinline__ void blend_staged(const float* __restrict__ box, const int lo[3], const int n[3],
                                              uint32_t res, const float x[3], float feat[F]) {
   Cell cell = level_cell(x, res);
+  const float ox = 1.f - cell.w[0], oy = 1.f - cell.w[1];
+  const float wxy[4] = {ox * oy, cell.w[0] * oy, ox * cell.w[1], cell.w[0] * cell.w[1]};
+  const float wz[2] = {1.f - cell.w[2], cell.w[2]};
+  const int n0 = n[0], n01 = n[0] * n[1];
+  const float* e0 = box + ((int)cell.i[0] - lo[0] + n0 * ((int)cell.i[1] - lo[1] + n[1] * ((int)cell.i[2] - lo[2]))) * F;
 #pragma unroll
   for (int f = 0; f < F; ++f) feat[f] = 0.f;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const int vx = (int)cell.i[0] + (c & 1) - lo[0];
-    const int vy = (int)cell.i[1] + ((c >> 1) & 1) - lo[1];
-    const int vz = (int)cell.i[2] + ((c >> 2) & 1) - lo[2];
-    const float* e = box + (vx + n[0] * (vy + n[1] * vz)) * F;
-    const float w = corner_weight(cell, c);
+    const float* e = e0 + ((c & 1) + ((c >> 1) & 1) * n0 + (c >> 2) * n01) * F;
+    const float w = wxy[c & 3] * wz[c >> 2];
 #pragma unroll
     for (int f = 0; f < F; ++f) feat[f] = fmaf(w, e[f], feat[f]);
   }
@@ -750,7 +757,8 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
       valid = jx < a.cnt[0] && jy < a.cnt[1] && jz < a.cnt[2];
       const int jj[3] = {min(jx, a.cnt[0] - 1), min(jy, a.cnt[1] - 1), min(jz, a.cnt[2] - 1)};
 #pragma unroll
-      for (int d = 0; d < 3; ++d) x[d] = __fdiv_rn((float)jj[d], (float)a.res[d]);
+      for (int d = 0; d < 3; ++d)
+        x[d] = a.rinv[d] != 0.f ? (float)jj[d] * a.rinv[d] : __fdiv_rn((float)jj[d], (float)a.res[d]);
       if (md.mesh[0]) {   // rectilinear (R36): the block's nodes (no staging: nst = 0)
 #pragma unroll
         for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
@@ -810,8 +818,10 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
           for (int u = 0; u < NB; ++u)
             if (l0 + 2 * u < net.L) {
               const LevelInfo& lv = net.lv[l0 + 2 * u];
-              const Cell cell = level_cell(x, lv.res);
-              e[u] = load_entry<F>(P + lv.offset + (size_t)corner_index(cell, 0, lv, net.table_mask) * F);
+              const float N = (float)lv.res;
+              const uint32_t v0 = (uint32_t)__fmul_rn(x[0], N), v1 = (uint32_t)__fmul_rn(x[1], N),
+                             v2 = (uint32_t)__fmul_rn(x[2], N);
+              e[u] = load_entry<F>(P + lv.offset + (size_t)vertex_index(v0, v1, v2, lv, net.table_mask) * F);
             }
         };
         auto consume = [&](int l0) {
@@ -1042,6 +1052,7 @@ void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res
     if (!al) break;
     a.na = l;
   }
+  for (int d = 0; d < 3; ++d) a.rinv[d] = (res[d] & (res[d] - 1)) == 0 ? 1.f / (float)res[d] : 0.f;
   const long long nb = (long long)((cnt[0] + kBrickX - 1) / kBrickX) * ((cnt[1] + kBrickY - 1) / kBrickY) *
                        ((cnt[2] + kBrickZ - 1) / kBrickZ);
   launch_forward<1>(*single_group(net, md), a, nb, st);

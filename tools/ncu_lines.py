@@ -1,14 +1,15 @@
 """Per-CUDA-source-line instruction and stall-sample totals from an ncu report
 (ncu -i REP --page source --csv --print-source cuda,sass).
 
-  python tools/ncu_lines.py REP [per-unit divisor] [top N]
+  python tools/ncu_lines.py REP [per-unit divisor] [top N] [kernel-name regex]
 """
 import csv, io, subprocess, sys
 
 rep = sys.argv[1]
 div = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilt = ["-k", "regex:" + sys.argv[4]] if len(sys.argv) > 4 else []
+out = subprocess.run(["ncu", "-i", rep] + kfilt + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname, cur, hdr = None, None, None
