@@ -168,7 +168,13 @@ INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
  *   sparse_adam != 0 (default 0; NEXT-4, a flagged semantics change versus
  *   R12, DESIGN R37): a hash-table parameter is updated only if its aligned
  *   group of 8 table floats (one 32-B sector) received a non-zero gradient this
- *   step; untouched groups keep p, m and v.  MLP parameters stay dense. */
+ *   step; untouched groups keep p, m and v.  MLP parameters stay dense.
+ *   split_step != 0 (default 1): a call that fits one launch group of >= 2 fp16
+ *   models on a stream without PSNR-target stopping runs each step as two
+ *   halves of the group, and each half's Adam runs beside the other half's
+ *   tensor-core MLP ("split fit step").  Every model takes the same
+ *   operations in the same order as with split_step = 0, so the deterministic
+ *   reduction mode gives bitwise the same parameters either way. */
 typedef struct {
   double lambda;
   int32_t boundary_batch;
@@ -180,6 +186,7 @@ typedef struct {
   int32_t check_interval;
   double vmin_c[INR_MAX_CHANNELS], vmax_c[INR_MAX_CHANNELS];
   int32_t sparse_adam;        /* R37: touched-only table updates (0 = dense PyTorch Adam) */
+  int32_t split_step;         /* 1 (default): split fit step, see below; 0: one pipeline */
 } inr_fit_opts;
 INR_API void inr_fit_opts_default(inr_fit_opts* o);
 

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <deque>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -545,6 +546,7 @@ extern "C" void inr_fit_opts_default(inr_fit_opts* o) {
   o->target_psnr = 0.0;
   o->check_interval = 0;
   o->sparse_adam = 0;
+  o->split_step = 1;
 }
 
 // Make sure device-resident parameters exist for a (possibly host-resident) model.
@@ -660,6 +662,7 @@ static void keep_pool(int device) {
 struct FitGraph {
   std::vector<unsigned char> key;
   cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec_first = nullptr;   // split step: the first step of a call (no deferred Adam)
   void* ws = nullptr;
   int device = -1;
   unsigned long long last_use = 0;
@@ -670,14 +673,56 @@ static std::list<FitGraph> g_graphs;
 static unsigned long long g_graph_clock = 0;
 constexpr size_t kGraphCache = 4;
 
+// ---- split fit step (one group of >= 2 models, CUDA graphs): the group's two halves
+// A and B run the pipeline in turn, and each half's Adam (HBM-bound) runs on a second
+// stream beside the other half's tensor-core MLP (latency-bound), on the SMs' spare
+// registers and warps:
+//   fwd_A prep_A {mlp_A | adam_B(s-1)} bwd_A fwd_B prep_B {mlp_B | adam_A(s)} bwd_B
+// Half B's Adam of the last step is flushed at the end of the call.  Per model the
+// order of operations is the unsplit step's (blocks are independent).
+static GroupArgs sub_group(const GroupArgs& g, int j0, int n) {
+  GroupArgs s;
+  memset(&s, 0, sizeof s);
+  s.net = g.net;
+  s.nmodels = n;
+  for (int j = 0; j < n; ++j) s.md[j] = g.md[j0 + j];
+  return s;
+}
+
+static LmWorkspace sub_workspace(const LmWorkspace& w, const NetDesc& net, int j0) {
+  LmWorkspace s = w;
+  s.samples += (size_t)j0 * w.Bs;
+  s.featimg += (size_t)j0 * (w.Bs / 128) * w.geom.tile_bytes;
+  s.dfeat += (size_t)j0 * w.Bs * net.LF;
+  s.wimg += (size_t)j0 * w.img_bytes;
+  if (s.targets) s.targets += (size_t)j0 * w.Bs;
+  return s;
+}
+
+// the side stream and fork / join events of the split step while it is captured
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  SideStream() {
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  ~SideStream() {
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(s);
+  }
+};
+
 static void free_graph(FitGraph& f) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(f.device);
   if (f.exec) cudaGraphExecDestroy(f.exec);
+  if (f.exec_first) cudaGraphExecDestroy(f.exec_first);
   if (f.ws) cudaFree(f.ws);
   cudaSetDevice(cur);
   f.exec = nullptr;
+  f.exec_first = nullptr;
   f.ws = nullptr;
 }
 
@@ -802,6 +847,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   const bool graphs = st != nullptr && !probing;
   const bool whole = graphs && g_prof_on && steps >= 2;
   const bool cached = graphs && !whole;
+  const bool split = tc && graphs && nchunks == 1 && groups[0].nmodels >= 2 && opts->split_step != 0;
   const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
   const int per = std::min(nmodels, kMaxGroup);
   const size_t ws_bytes = tc ? lm_workspace_bytes(m0->net, per, Bs) : 0;
@@ -811,7 +857,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       const unsigned char* b = (const unsigned char*)p;
       key.insert(key.end(), b, b + n);
     };
-    int hdr[5] = {m0->device, (int)tc, Bs, nchunks, (int)ws_bytes};
+    int hdr[6] = {m0->device, (int)tc, Bs, nchunks, (int)ws_bytes, (int)split};
     put(hdr, sizeof hdr);
     put(&fs, sizeof fs);
     put(&as, sizeof as);
@@ -841,6 +887,45 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     else { CK(cudaMallocAsync(&ws_mem, ws_bytes, st)); ws_base = ws_mem; }
   }
   if (tc) ws = lm_workspace(ws_base, m0->net, per, Bs);
+  GroupArgs gh[2];
+  LmWorkspace wh[2];
+  if (split) {
+    const int h = groups[0].nmodels / 2;
+    gh[0] = sub_group(groups[0], 0, h);
+    gh[1] = sub_group(groups[0], h, groups[0].nmodels - h);
+    wh[0] = sub_workspace(ws, m0->net, 0);
+    wh[1] = sub_workspace(ws, m0->net, h);
+  }
+  // beside each other: one MLP CTA (256 threads, half the registers) and one TMA-fed Adam
+  // CTA (512 threads, 96 KB of operands in flight) per SM
+  constexpr int kSplitMlpCtas = 148, kSplitAdamCtas = 148;
+  auto enqueue_split = [&](cudaStream_t s, const SideStream& side, bool first) {
+    for (int hf = 0; hf < 2; ++hf) {
+      const GroupArgs& g = gh[hf];
+      const LmWorkspace& w = wh[hf];
+      const GroupArgs& o = gh[hf ^ 1];
+      { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, w, s); }
+      { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, w.wimg, s); }
+      const bool side_adam = hf == 1 || !first;   // the other half's Adam (of the previous step for B)
+      if (side_adam) {
+        cudaEventRecord(side.ev[2 * hf], s);
+        cudaStreamWaitEvent(side.s, side.ev[2 * hf], 0);
+        { ProfScope p(PK_ADAM, side.s); launch_adam(o, o.nmodels, as, side.s, kSplitAdamCtas); }
+      }
+      { ProfScope p(PK_MLP_TC, s);
+        launch_mlp_tc(g, g.nmodels, fs, w.featimg, w.wimg, w.samples, w.targets, w.dfeat, w.Bs, s,
+                      side_adam ? kSplitMlpCtas : 0); }
+      if (side_adam) {
+        cudaEventRecord(side.ev[2 * hf + 1], side.s);
+        cudaStreamWaitEvent(s, side.ev[2 * hf + 1], 0);
+      }
+      { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, w, s); }
+    }
+  };
+  auto flush_split = [&](cudaStream_t s) {   // half B's Adam of the last step
+    ProfScope p(PK_ADAM, s);
+    launch_adam(gh[1], gh[1].nmodels, as, s);
+  };
   auto enqueue_step = [&](cudaStream_t s) {
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
@@ -863,20 +948,31 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     void*& p; cudaStream_t s;
     ~WsFree() { if (p) cudaFreeAsync(p, s); }
   } ws_free{ws_mem, st};
+  cudaGraphExec_t exec_first = entry ? entry->exec_first : nullptr;
   if (graphs && !exec) {
-    cudaGraph_t graph;
-    {
-      cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-      if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamBeginCapture"); }
+    // variant 0: the step (steady split step); variant 1: the split step of a call's first step
+    std::unique_ptr<SideStream> side(split ? new SideStream() : nullptr);
+    for (int variant = 0; variant < (split && !whole ? 2 : 1); ++variant) {
+      cudaGraph_t graph;
+      {
+        cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamBeginCapture"); }
+      }
+      long long before = g_launches.load();
+      for (int s = 0; s < (whole ? steps : 1); ++s) {
+        if (split) enqueue_split(st, *side, whole ? s == 0 : variant == 1);
+        else enqueue_step(st);
+      }
+      if (split && whole) flush_split(st);
+      g_launches.store(before);  // captured launches are counted per replay below
+      cudaError_t e = cudaStreamEndCapture(st, &graph);
+      if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamEndCapture"); }
+      cudaGraphExec_t x = nullptr;
+      e = cudaGraphInstantiate(&x, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaGraphInstantiate"); }
+      (variant == 0 ? exec : exec_first) = x;
     }
-    long long before = g_launches.load();
-    for (int s = 0; s < (whole ? steps : 1); ++s) enqueue_step(st);
-    g_launches.store(before);  // captured launches are counted per replay below
-    cudaError_t e = cudaStreamEndCapture(st, &graph);
-    if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaStreamEndCapture"); }
-    e = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) { if (cached) cudaFree(ws_base); return cuda_fail(e, "cudaGraphInstantiate"); }
     if (cached) {   // insert, evicting the least recently used idle entry beyond kGraphCache
       if (g_graphs.size() >= kGraphCache) {
         auto lru = g_graphs.end();
@@ -890,6 +986,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       FitGraph f;
       f.key = key;
       f.exec = exec;
+      f.exec_first = exec_first;
       f.ws = ws_base;
       f.device = m0->device;
       f.last_use = ++g_graph_clock;
@@ -913,12 +1010,13 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   for (int s = 0; s < steps; ++s) {
     if (exec) {
       if (whole && s > 0) { taken = s + 1; continue; }
-      cudaError_t e = cudaGraphLaunch(exec, st);
+      cudaError_t e = cudaGraphLaunch(s == 0 && exec_first ? exec_first : exec, st);
       if (e != cudaSuccess) {
         if (!cached) cudaGraphExecDestroy(exec);
         return cuda_fail(e, "cudaGraphLaunch");
       }
-      count_launch((long long)launches_per_step * (whole ? steps : 1));
+      // (split: 10 launches per step, 9 in a call's first, + the final Adam flush)
+      count_launch(split ? (whole ? 10ll * steps : (s == 0 ? 9 : 10)) : (long long)launches_per_step * (whole ? steps : 1));
     } else {
       enqueue_step(st);
       CK_LAUNCH("fit step");
@@ -948,7 +1046,9 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       }
     }
   }
+  if (split && !whole) flush_split(st);   // (counts its own launch)
   if (exec && !cached) cudaGraphExecDestroy(exec);
+  if (exec_first && !cached) cudaGraphExecDestroy(exec_first);
   for (int i = 0; i < nmodels; ++i) {
     if (steps_of[i] < 0) steps_of[i] = taken;
     models[i]->steps += steps_of[i];

@@ -11,6 +11,7 @@
 #include "adam.cuh"
 #include "common.cuh"
 #include "launch.h"
+#include "tc_common.cuh"
 
 namespace inr {
 
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kTile) fit_simt_kernel(GroupArgs g, FitScalars
 // PyTorch torch.optim.Adam (R12): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
 // p -= (lr/bc1) m / (sqrt(v)/sqrt(bc2) + eps); lr = lr0 decay^floor(s/lr_step) (R13).
 // Deterministic mode converts the exact int64 sums to fp32 first.
+template <int SIDE>   // SIDE: launched beside the MLP (its own carveout attribute)
 __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
   const ModelDev& md = g.md[blockIdx.y];
   const AdamStep a = adam_step_scalars(*md.step_cur, as.lr0, as.lr_decay, as.lr_step, as.beta1, as.beta2, as.b1,
@@ -281,6 +283,90 @@ __global__ void adam_kernel(GroupArgs g, AdamScalars as) {
                                    adam_range(md, a, as.table_end, g.net.nparams, tid, nth)
                              : adam_range(md, a, 0, g.net.nparams, tid, nth);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(md.flag, 1);
+}
+
+// Adam with its operands streamed by TMA bulk copies (same arithmetic as adam4): each
+// CTA owns a contiguous run of chunks of one model's p, g, m, v, kept STAGES deep in
+// flight in shared memory instead of in registers, so a few warps per SM keep HBM
+// busy -- the split fit step runs it on the SMs' spare warps beside the tensor-core
+// MLP (whose CTAs hold half the register file).  Per stage a "full" mbarrier (the
+// bulk copies' bytes) and an "empty" one (one arrival per warp done with it): the
+// warps run ahead independently; only the issuing thread waits for a stage to drain.
+// Plain fp32 gradients only (the deterministic mode and R37 use adam_kernel).
+constexpr size_t adam_tma_smem(int chunk, int stages) { return (size_t)stages * 4 * chunk * 4 + stages * 16; }
+
+template <int THREADS, int CHUNK, int STAGES>
+__global__ void __launch_bounds__(THREADS) adam_tma_kernel(GroupArgs g, AdamScalars as) {
+  extern __shared__ __align__(128) uint8_t adam_smem[];
+  constexpr int kWarps = THREADS / 32, C4 = CHUNK / 4;
+  const ModelDev& md = g.md[blockIdx.y];
+  const AdamStep a = adam_step_scalars(*md.step_cur, as.lr0, as.lr_decay, as.lr_step, as.beta1, as.beta2, as.b1,
+                                       as.b2, as.ob1, as.ob2, as.eps);
+  const int t = threadIdx.x;
+  float* stage = reinterpret_cast<float*>(adam_smem);   // [stage][p, g, m, v][CHUNK]
+  const uint32_t full0 = tc::smem_u32(adam_smem + (size_t)STAGES * 4 * CHUNK * 4);
+  const uint32_t empty0 = full0 + 8 * STAGES;
+  const long long n = g.net.nparams;
+  const long long nch = (n + CHUNK - 1) / CHUNK;
+  const long long per = (nch + gridDim.x - 1) / gridDim.x;
+  const long long c0 = (long long)blockIdx.x * per, c1 = min(nch, c0 + per);
+  if (t == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(full0 + 8 * s, 1);
+      tc::mbar_init(empty0 + 8 * s, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const float* src[4] = {md.params, md.grads, md.adam_m, md.adam_v};
+  auto issue = [&](long long c) {
+    const int s = (int)((c - c0) % STAGES);
+    const long long off = c * CHUNK;
+    const uint32_t bytes = (uint32_t)(min((long long)CHUNK, n - off) * 4);
+    tc::fence_async_smem();   // the stage's previous contents were read by the generic proxy
+    tc::mbar_expect_tx(full0 + 8 * s, 4 * bytes);
+    for (int q = 0; q < 4; ++q)
+      tc::bulk_g2s(tc::smem_u32(stage + ((size_t)s * 4 + q) * CHUNK), src[q] + off, bytes, full0 + 8 * s);
+  };
+  if (t == 0)
+    for (long long c = c0; c < min(c1, c0 + STAGES - 1); ++c) issue(c);
+  float4* __restrict__ P = reinterpret_cast<float4*>(md.params);
+  float4* __restrict__ M = reinterpret_cast<float4*>(md.adam_m);
+  float4* __restrict__ V = reinterpret_cast<float4*>(md.adam_v);
+  bool bad = false;
+  for (long long c = c0; c < c1; ++c) {
+    const long long u = c - c0;
+    const int s = (int)(u % STAGES);
+    if (t == 0 && c + STAGES - 1 < c1) {
+      // chunk c + S - 1 goes where chunk c - 1 was: wait until every warp is done with it
+      if (u > 0) tc::mbar_wait(empty0 + 8 * (int)((u - 1) % STAGES), (uint32_t)(((u - 1) / STAGES) & 1));
+      issue(c + STAGES - 1);
+    }
+    tc::mbar_wait(full0 + 8 * s, (uint32_t)((u / STAGES) & 1));
+    const float4* sp = reinterpret_cast<const float4*>(stage + (size_t)s * 4 * CHUNK);
+    const long long base = c * C4;
+    const int cnt4 = (int)(min((long long)CHUNK, n - c * CHUNK) / 4);
+#pragma unroll
+    for (int k = 0; k < (C4 + THREADS - 1) / THREADS; ++k) {
+      const int e = t + k * THREADS;
+      if (e < cnt4) {
+        float4 pp = sp[e], gg = sp[C4 + e], mm = sp[2 * C4 + e], vv = sp[3 * C4 + e];
+#define ADAM1(c)                                                                  \
+  mm.c = fmaf(a.b1, mm.c, a.ob1 * gg.c);                                          \
+  vv.c = fmaf(a.b2, vv.c, a.ob2 * gg.c * gg.c);                                   \
+  pp.c = pp.c - a.step_size * mm.c / (sqrtf(vv.c) * a.inv_sqrt_bc2 + a.eps);      \
+  bad |= !isfinite(pp.c);
+        ADAM1(x) ADAM1(y) ADAM1(z) ADAM1(w)
+#undef ADAM1
+        M[base + e] = mm;
+        V[base + e] = vv;
+        P[base + e] = pp;
+      }
+    }
+    __syncwarp();
+    if ((t & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(empty0 + 8 * s) : "memory");
+  }
+  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(md.flag, 1);
 }
 
 // ------------------------------------------------------------- decode grid
@@ -531,10 +617,27 @@ void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cuda
   count_launch();
 }
 
-void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st) {
+void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st, int ctas) {
+  if (ctas > 0) {
+    // beside the MLP (split fit step): the MLP's shared-memory carveout, so that an SM
+    // running the MLP CTA also takes these (a carveout change waits for the SM to drain)
+    const int bx = std::max(1, (ctas + nmodels - 1) / nmodels);
+    if (!as.sparse && !g.md[0].grads_fx) {
+      constexpr int kT = 512, kC = 2048, kS = 3;   // 96 KB of operands in flight per CTA
+      cudaFuncSetAttribute(adam_tma_kernel<kT, kC, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)adam_tma_smem(kC, kS));
+      cudaFuncSetAttribute(adam_tma_kernel<kT, kC, kS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      adam_tma_kernel<kT, kC, kS><<<dim3(bx, nmodels), kT, adam_tma_smem(kC, kS), st>>>(g, as);
+    } else {
+      cudaFuncSetAttribute(adam_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      adam_kernel<1><<<dim3(bx, nmodels), 256, 0, st>>>(g, as);
+    }
+    count_launch();
+    return;
+  }
   long long per = (g.net.nparams / 4 + 255) / 256;
   int bx = (int)std::max<long long>(1, std::min<long long>(per, (148 * 8 + nmodels - 1) / nmodels));
-  adam_kernel<<<dim3(bx, nmodels), 256, 0, st>>>(g, as);
+  adam_kernel<0><<<dim3(bx, nmodels), 256, 0, st>>>(g, as);
   count_launch();
 }
 

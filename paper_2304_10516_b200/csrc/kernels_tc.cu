@@ -567,12 +567,12 @@ void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStrea
 }
 
 void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
-                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st) {
+                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st, int ctas) {
   Layout L;
   if (!build_layout(g.net, L)) return;
   const int total = fs.B_u + fs.B_b;
   const int ntiles = (total + kTileM - 1) / kTileM;
-  const int slots = 148 * L.ctas_per_sm;
+  const int slots = ctas > 0 ? ctas : 148 * L.ctas_per_sm;
   // CTAs per model: fill the machine; in the deterministic mode a fixed count, so
   // that the tiles each CTA accumulates in fp32 TMEM (and hence the exact result)
   // do not depend on how many models share the launch

@@ -101,7 +101,8 @@ void launch_init_params(const NetDesc& net, float* params, uint32_t k0, uint32_t
                         cudaStream_t st);
 void launch_step_begin(const GroupArgs& g, int nmodels, long long zero_from, cudaStream_t st);
 void launch_fit_simt(const GroupArgs& g, int nmodels, const FitScalars& fs, cudaStream_t st);
-void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st);
+// ctas > 0: total CTAs of the launch (the split fit step runs it beside an MLP launch)
+void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStream_t st, int ctas = 0);
 void launch_probe(const GroupArgs& g, int nmodels, cudaStream_t st);
 void launch_decode_grid_simt(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,
                              const long long os[3], const float* ref, double* sse, cudaStream_t st);
@@ -144,7 +145,8 @@ void launch_encode_fwd(const GroupArgs& g, int nmodels, const FitScalars& fs, co
 void launch_encode_bwd(const GroupArgs& g, int nmodels, const FitScalars& fs, const LmWorkspace& w, cudaStream_t st);
 bool tc_supported(const NetDesc& net);
 void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const uint8_t* featimg, const uint8_t* wimg,
-                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st);
+                   const float4* samples, const float4* targets, float* dfeat, int Bs, cudaStream_t st,
+                   int ctas = 0);   // ctas > 0: at most this many CTAs in all (deterministic mode: ignored)
 void launch_debug_forward_tc(const NetDesc& net, const float* P, const float* x01, long long q, float* y,
                              cudaStream_t st);
 void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res[3], const int cnt[3], float* out,

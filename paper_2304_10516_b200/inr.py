@@ -52,7 +52,8 @@ class inr_fit_opts(ctypes.Structure):
                 ("lr_decay", ctypes.c_double), ("lr_step", ctypes.c_int32), ("beta1", ctypes.c_double),
                 ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("vmin", ctypes.c_double),
                 ("vmax", ctypes.c_double), ("target_psnr", ctypes.c_double), ("check_interval", ctypes.c_int32),
-                ("vmin_c", ctypes.c_double * 3), ("vmax_c", ctypes.c_double * 3), ("sparse_adam", ctypes.c_int32)]
+                ("vmin_c", ctypes.c_double * 3), ("vmax_c", ctypes.c_double * 3), ("sparse_adam", ctypes.c_int32),
+                ("split_step", ctypes.c_int32)]
 
     def set_range(self, lo, hi):
         """Scalar range (scalar fields) or per-channel sequences (vector fields)."""

@@ -1,0 +1,115 @@
+"""The split fit step (inr_fit_opts.split_step): a group's two halves
+run the level-major pipeline in turn and each half's Adam runs beside the other
+half's tensor-core MLP, half B's last Adam deferred to the end of the call.
+Per model the operations and their order are the unsplit step's (blocks are
+independent), so
+
+  * in the deterministic reduction mode the parameters and Adam moments of a
+    multi-step split fit are bitwise those of the unsplit fit (any misrouted
+    workspace, skipped or doubled Adam shows up here), and
+  * the TMA-fed Adam kernel that runs beside the MLP (plain fp32 gradients)
+    is the PyTorch-form Adam of R12: each step's GPU gradient fed to the
+    oracle's adam_update reproduces p, m, v to fp32 rounding (as
+    test_gpu_parity.test_adam_elementwise_across_lr_decays)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import adam as o_adam, sampler
+from paper_2304_10516_b200 import inr
+
+from gpu_util import gpu_volume, get_grads, get_params, make_gpu_model, stream, whole_view
+
+pytestmark = pytest.mark.gpu
+
+CFG1 = dict(levels=8, features=2, log2_table_size=14, mlp_hidden_layers=2)
+
+
+def _setup(n_models, reduction, seed0=11):
+    vol = synth.g1_analytic(32).numpy()
+    blocks = sampler.decompose((32, 32, 32), (16, 16, 16))[:n_models]
+    lo, hi = sampler.value_range([vol])
+    vt = gpu_volume(vol)
+    models = [make_gpu_model(b, seed0 + i, reduction=reduction, precision=inr.INR_PREC_FP16_MLP, **CFG1)
+              for i, b in enumerate(blocks)]
+    go = inr.inr_fit_opts_default()
+    go.vmin, go.vmax, go.boundary_batch, go.lr_step = lo, hi, 256, 3
+    return vt, models, go
+
+
+def _state(m):
+    p = get_params(m)
+    mm, vv = inr.inr_get_adam_state(m, np.empty_like(p), np.empty_like(p))
+    return p, mm, vv
+
+
+@pytest.mark.parametrize("n_models", [2, 5])
+def test_split_step_bitwise_equals_unsplit_deterministic(n_models):
+    """5 models: halves of 2 and 3.  Two calls (7 + 4 steps: the first-step and
+    steady-step graphs, the final flush of half B's Adam, LR decays at s = 3, 6, 9)."""
+    out = []
+    for split in (1, 0):
+        vt, models, go = _setup(n_models, reduction=1)
+        go.split_step = split
+        views = [whole_view(vt)] * n_models
+        for steps in (7, 4):
+            inr.inr_fit_group(models, views, steps, 1024, go, stream())
+        out.append([_state(m) for m in models] + [[inr.inr_steps(m) for m in models]])
+        for m in models:
+            inr.inr_destroy(m)
+    a, b = out
+    assert a[-1] == b[-1] == [11] * n_models
+    for i in range(n_models):
+        for x, y in zip(a[i], b[i]):
+            assert np.array_equal(x, y), i
+
+
+def test_split_step_tma_adam_elementwise():
+    """Two models, plain fp32 gradients: in a one-step split call model 0's Adam
+    is the TMA-fed kernel beside model 1's MLP, model 1's the final flush (the
+    standalone kernel); both checked element by element against the oracle's
+    Adam over 6 steps crossing two LR decays."""
+    vt, models, go = _setup(2, reduction=0)
+    views = [whole_view(vt)] * 2
+    ref = []
+    for m in models:
+        p = get_params(m).astype(np.float64)
+        ref.append([p, np.zeros_like(p), np.zeros_like(p), np.zeros_like(p)])
+    worst = 0.0
+    for t in range(1, 7):
+        inr.inr_fit_group(models, views, 1, 1024, go, stream())
+        for m, (p, mo, vo, gmax) in zip(models, ref):
+            g = get_grads(m).astype(np.float64)
+            assert np.any(g != 0)
+            np.maximum(gmax, np.abs(g), out=gmax)
+            o_adam.adam_update(p, g, mo, vo, t, o_adam.lr_at(t - 1, 1e-2, 0.8, 3))
+            pg, mg, vg = _state(m)
+            tol_p = t * (1e-6 * 1e-2 + 2.0 ** -21 * np.abs(p))
+            tol_m = t * 2.0 ** -21 * gmax
+            tol_v = t * 2.0 ** -21 * vo + 1e-37
+            r = [float(np.max(np.abs(pg - p) / tol_p)), float(np.max(np.abs(mg - mo) / tol_m.clip(1e-30))),
+                 float(np.max(np.abs(vg - vo) / tol_v))]
+            worst = max(worst, max(r))
+            assert max(r) <= 1, (t, r)
+    print("split step, TMA Adam: worst error / tolerance", worst)
+    for m in models:
+        inr.inr_destroy(m)
+
+
+def test_split_step_multistep_matches_unsplit_statistically():
+    """Plain fp32 gradients (atomic reduction order varies run to run): a 40-step
+    split fit of 4 models ends at the unsplit fit's loss to within the run-to-run
+    spread (the TMA Adam of the steady graph included; elementwise agreement is
+    the deterministic test's job)."""
+    res = []
+    for split in (1, 0):
+        vt, models, go = _setup(4, reduction=0)
+        go.split_step = split
+        reps = inr.inr_fit_group(models, [whole_view(vt)] * 4, 40, 1024, go, stream())
+        res.append(([r.loss_uniform for r in reps], [get_params(m) for m in models]))
+        for m in models:
+            inr.inr_destroy(m)
+    (la, pa), (lb, pb) = res
+    for x, y in zip(la, lb):
+        assert abs(x - y) <= 0.05 * max(x, y), (la, lb)
+    assert all(np.isfinite(x).all() for x in pa)
