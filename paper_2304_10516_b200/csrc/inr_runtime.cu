@@ -702,7 +702,7 @@ static LmWorkspace sub_workspace(const LmWorkspace& w, const NetDesc& net, int j
 // the side stream and fork / join events of the split step while it is captured
 struct SideStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {};
   SideStream() {
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -899,26 +899,32 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   // beside each other: one MLP CTA (256 threads, half the registers) and one TMA-fed Adam
   // CTA (512 threads, 96 KB of operands in flight) per SM
   constexpr int kSplitMlpCtas = 148, kSplitAdamCtas = 148;
+  // fork / join between the launching stream and the side stream (inside a capture)
+  auto fork = [](cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
+    cudaEventRecord(e, from);
+    cudaStreamWaitEvent(to, e, 0);
+  };
   auto enqueue_split = [&](cudaStream_t s, const SideStream& side, bool first) {
     for (int hf = 0; hf < 2; ++hf) {
       const GroupArgs& g = gh[hf];
       const LmWorkspace& w = wh[hf];
       const GroupArgs& o = gh[hf ^ 1];
+      // this half's weight image on the side stream beside its encode: it needs this half's
+      // Adam of the previous step, which the side stream ran before it
+      fork(s, side.s, side.ev[4 * hf]);
+      { ProfScope p(PK_PREP, side.s); launch_prep_image(g, g.nmodels, w.wimg, side.s); }
+      cudaEventRecord(side.ev[4 * hf + 1], side.s);
       { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, w, s); }
-      { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, w.wimg, s); }
+      cudaStreamWaitEvent(s, side.ev[4 * hf + 1], 0);
       const bool side_adam = hf == 1 || !first;   // the other half's Adam (of the previous step for B)
       if (side_adam) {
-        cudaEventRecord(side.ev[2 * hf], s);
-        cudaStreamWaitEvent(side.s, side.ev[2 * hf], 0);
+        fork(s, side.s, side.ev[4 * hf + 2]);
         { ProfScope p(PK_ADAM, side.s); launch_adam(o, o.nmodels, as, side.s, kSplitAdamCtas); }
       }
       { ProfScope p(PK_MLP_TC, s);
         launch_mlp_tc(g, g.nmodels, fs, w.featimg, w.wimg, w.samples, w.targets, w.dfeat, w.Bs, s,
                       side_adam ? kSplitMlpCtas : 0); }
-      if (side_adam) {
-        cudaEventRecord(side.ev[2 * hf + 1], side.s);
-        cudaStreamWaitEvent(s, side.ev[2 * hf + 1], 0);
-      }
+      if (side_adam) fork(side.s, s, side.ev[4 * hf + 3]);
       { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, w, s); }
     }
   };
@@ -926,14 +932,21 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
     ProfScope p(PK_ADAM, s);
     launch_adam(gh[1], gh[1].nmodels, as, s);
   };
-  auto enqueue_step = [&](cudaStream_t s) {
+  auto enqueue_step = [&](cudaStream_t s, const SideStream* side) {
     for (int c = 0; c < nchunks; ++c) {
       const GroupArgs& g = groups[c];
       if (tc) {
-        // (encode_fwd zeroes the gradient and draws the step's samples; prep_image then
-        // advances the step counters: no separate step_begin launch)
+        // (encode_fwd zeroes the gradient and the loss sums and draws the step's samples with
+        // step_total, encode_bwd advances the step counters for Adam: no step_begin launch;
+        // captured, the weight image is prepared on the side stream beside encode_fwd)
+        if (side) {
+          fork(s, side->s, side->ev[0]);
+          { ProfScope p(PK_PREP, side->s); launch_prep_image(g, g.nmodels, ws.wimg, side->s); }
+          cudaEventRecord(side->ev[1], side->s);
+        }
         { ProfScope p(PK_ENCODE_FWD, s); launch_encode_fwd(g, g.nmodels, fs, ws, s); }
-        { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
+        if (side) cudaStreamWaitEvent(s, side->ev[1], 0);
+        else { ProfScope p(PK_PREP, s); launch_prep_image(g, g.nmodels, ws.wimg, s); }
         { ProfScope p(PK_MLP_TC, s); launch_mlp_tc(g, g.nmodels, fs, ws.featimg, ws.wimg, ws.samples, ws.targets, ws.dfeat, ws.Bs, s); }
         { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, ws, s); }
         { ProfScope p(PK_ADAM, s); launch_adam(g, g.nmodels, as, s); }
@@ -951,7 +964,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   cudaGraphExec_t exec_first = entry ? entry->exec_first : nullptr;
   if (graphs && !exec) {
     // variant 0: the step (steady split step); variant 1: the split step of a call's first step
-    std::unique_ptr<SideStream> side(split ? new SideStream() : nullptr);
+    std::unique_ptr<SideStream> side(tc ? new SideStream() : nullptr);
     for (int variant = 0; variant < (split && !whole ? 2 : 1); ++variant) {
       cudaGraph_t graph;
       {
@@ -961,7 +974,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       long long before = g_launches.load();
       for (int s = 0; s < (whole ? steps : 1); ++s) {
         if (split) enqueue_split(st, *side, whole ? s == 0 : variant == 1);
-        else enqueue_step(st);
+        else enqueue_step(st, side.get());
       }
       if (split && whole) flush_split(st);
       g_launches.store(before);  // captured launches are counted per replay below
@@ -1018,7 +1031,7 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       // (split: 10 launches per step, 9 in a call's first, + the final Adam flush)
       count_launch(split ? (whole ? 10ll * steps : (s == 0 ? 9 : 10)) : (long long)launches_per_step * (whole ? steps : 1));
     } else {
-      enqueue_step(st);
+      enqueue_step(st, nullptr);
       CK_LAUNCH("fit step");
     }
     taken = s + 1;

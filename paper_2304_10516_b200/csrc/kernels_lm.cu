@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, Fit
       for (long long q = a + threadIdx.x; q < b; q += blockDim.x) g4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
+  if (blockIdx.x == 0 && l == 0 && threadIdx.x == 0) {   // this step's loss sums (the MLP adds to them)
+    md.acc[0] = 0.0;
+    md.acc[1] = 0.0;
+  }
   const int i = blockIdx.x * kLmThreads + threadIdx.x;
   if (i >= Bs) return;
   float f[F];
@@ -60,7 +64,7 @@ __global__ void __launch_bounds__(kLmThreads) encode_fwd_kernel(GroupArgs g, Fit
     // the sample is drawn here (Philox, R8) for every level; level 0's CTAs also
     // store it with its trilinear target(s) for the MLP and the scatter kernels
     float x[3];
-    // the step being executed: step_total, which prep_image_kernel advances after this kernel
+    // the step being executed: step_total, which encode_bwd_kernel advances
     draw_sample(md, i, fs.B_u, (uint32_t)*md.step_total, x);
     if (l == 0) {
       if (g.net.D == 1) {
@@ -167,6 +171,13 @@ __global__ void __launch_bounds__(kLmThreads) encode_bwd_kernel(GroupArgs g, Fit
   const int m = blockIdx.z, l = blockIdx.y;
   const ModelDev& md = g.md[m];
   const int total = fs.B_u + (md.nfaces > 0 ? fs.B_b : 0);
+  if (blockIdx.x == 0 && l == 0 && threadIdx.x == 0) {
+    // open the step for Adam: step_cur = the step executed (step_total, with which
+    // encode_fwd drew the samples), step_total += 1 (nothing else in the step reads them)
+    const long long s = *md.step_total;
+    *md.step_cur = s;
+    *md.step_total = s + 1;
+  }
   const int i0 = blockIdx.x * kBwdChunk;
   if (i0 >= total) return;
   scatter_chunk<F>(g, md, m, l, samples, dfeat, Bs, i0, min(i0 + kBwdChunk, total), acc_raw);

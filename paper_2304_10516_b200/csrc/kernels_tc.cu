@@ -71,21 +71,11 @@ __device__ __forceinline__ uint32_t mlp_setup_fit(const NetDesc& net, const uint
   return *tslot;
 }
 
-// Per step: each model's fp32 MLP weights -> the fp16 weight image (canonical
-// tiles + fp32 biases and output layer) that every fit CTA bulk-copies.
-// advance (fit): also opens the step of every model — step_cur = step_total, step_total
-// += 1, clear the loss sums — after encode_fwd has drawn its samples with step_total.
-__global__ void __launch_bounds__(256) prep_image_kernel(GroupArgs g, Layout lay, uint8_t* __restrict__ wimg,
-                                                         int advance) {
+// Per step (fit) or call (decode): each model's fp32 MLP weights -> the fp16 weight
+// image (canonical tiles + fp32 biases and output layer) that every CTA bulk-copies.
+// It reads only the parameters, so the fit runs it beside encode_fwd.
+__global__ void __launch_bounds__(256) prep_image_kernel(GroupArgs g, Layout lay, uint8_t* __restrict__ wimg) {
   const NetDesc& net = g.net;
-  if (advance && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
-    const ModelDev& md = g.md[blockIdx.x];
-    const long long s = *md.step_total;
-    *md.step_cur = s;
-    *md.step_total = s + 1;
-    md.acc[0] = 0.0;
-    md.acc[1] = 0.0;
-  }
   const float* __restrict__ P = g.md[blockIdx.x].params;
   uint8_t* dst = wimg + (size_t)blockIdx.x * lay.img_bytes;
   // CTA (model, y) converts rows y, y + gridDim.y, ... of every weight tile
@@ -562,7 +552,7 @@ bool tc_fit_geometry(const NetDesc& net, FeatGeom* geom, uint32_t* img_bytes) {
 void launch_prep_image(const GroupArgs& g, int nmodels, uint8_t* wimg, cudaStream_t st) {
   Layout L;
   if (!build_layout(g.net, L)) return;
-  prep_image_kernel<<<dim3(nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg, 1);
+  prep_image_kernel<<<dim3(nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg);
   count_launch();
 }
 
@@ -977,7 +967,7 @@ static void launch_forward(const GroupArgs& g, const FwdArgs& a0, long long ntil
   uint8_t* wimg = nullptr;   // the models' fp16 weight images (stream-ordered scratch)
   if (cudaMallocAsync((void**)&wimg, (size_t)g.nmodels * L.img_bytes, st) != cudaSuccess) return;
   a.wimg = wimg;
-  prep_image_kernel<<<dim3(g.nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg, 0);
+  prep_image_kernel<<<dim3(g.nmodels, 16), dim3(64, 4), 0, st>>>(g, L, wimg);
   count_launch();
   unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(ntiles_hint, 148ll * L.ctas_per_sm));
   switch (g.net.F * 10 + g.net.D) {
