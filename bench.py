@@ -240,7 +240,7 @@ def ncu_capture():
     capture (profiles/r2_ncu_full.txt, tools/ncu_summary.py format): DRAM bytes,
     L2 read / red sectors.  {bench kernel class: {...}}."""
     names = {"step_begin": "step_begin_kernel", "encode_fwd": "encode_fwd_kernel", "prep_image": "prep_image_kernel",
-             "mlp_tc": "mlp_fit_kernel", "encode_bwd": "encode_bwd_kernel", "adam": "adam_kernel"}
+             "mlp_tc": "mlp_fit_kernel", "encode_bwd": "encode_bwd_kernel", "adam": "adam_"}   # adam_tma_kernel
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     out, cur = {}, None
     try:
@@ -369,17 +369,23 @@ def run_ours(args):
     dom = max(kern, key=lambda k: kern[k][0])
     dom_ms, dom_n = kern[dom]
     avg_s = dom_ms / dom_n / 1e3
+    # blocks per launch: the split fit step launches each kernel once per half of the group
+    mpl = {k: nb * args.steps / v[1] for k, v in kern.items()}
     LF, W, H = CFG["levels"] * CFG["features"], 64, CFG["mlp_hidden_layers"]
     if dom == "adam":
         # algorithmic bytes: read p, g, m, v + write p, m, v (fp32) for every parameter of
-        # every block = 28 B/param (the gradient is zeroed by encode_fwd, charged there)
-        alg = 28.0 * P_int * nb
+        # the launch's blocks = 28 B/param (the gradient is zeroed by encode_fwd, charged there)
+        alg = 28.0 * P_int * mpl["adam"]
         roof = {"kernel": "adam", "bound": "hbm", "achieved": alg / avg_s / 1e9, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": alg,
                 "convention": "28 B/param/step (p, g, m, v read; p, m, v written); the 4 B/param gradient "
-                              "zeroing runs inside encode_fwd and is charged to the whole step below"}
+                              "zeroing runs inside encode_fwd and is charged to the whole step below",
+                "blocks_per_launch": mpl["adam"],
+                "note": "split fit step: each launch updates half of the blocks while the other half's MLP runs "
+                        "beside it on the same SMs (TMA-fed Adam, one CTA per SM); the time is that co-running "
+                        "launch's"}
     else:
-        flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step
+        flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step * mpl[dom] / nb
         peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
         roof = {"kernel": dom, "bound": "tensor", "achieved": flop / avg_s / 1e12, "peak": peak,
                 "unit": "TFLOP/s", "traffic": None, "algorithmic_flop_per_launch": flop}
@@ -393,7 +399,7 @@ def run_ours(args):
     roof["share_of_step"] = dom_ms / prof_span
     kernels = {k: {"total_ms": v[0], "launches": v[1], "avg_ms": v[0] / max(v[1], 1)} for k, v in kern.items()}
     # per-kernel fractions against each kernel's own bound
-    flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step
+    flop = 6.0 * (LF * W + (H - 1) * W * W + W) * coords_per_step * mpl.get("mlp_tc", nb) / nb
     if "mlp_tc" in kernels:
         tf = flop / (kernels["mlp_tc"]["avg_ms"] / 1e3) / 1e12
         kernels["mlp_tc"].update({"bound": "tensor", "achieved_tflops": tf,
@@ -413,8 +419,10 @@ def run_ours(args):
     except (OSError, KeyError, ValueError):
         pass
     if "adam" in kernels:
-        kernels["adam"].update({"bound": "hbm", "frac": 28.0 * P_int * nb / (kernels["adam"]["avg_ms"] / 1e3) / 1e9
-                                / pk["hbm_gbs"]})
+        kernels["adam"].update({"bound": "hbm", "frac": 28.0 * P_int * mpl["adam"] / (kernels["adam"]["avg_ms"] / 1e3)
+                                / 1e9 / pk["hbm_gbs"]})
+    for k in kernels:
+        kernels[k]["blocks_per_launch"] = mpl[k]
     # whole step: the algorithmic HBM bytes of one step (Adam 28 B/param + gradient zeroing
     # 4 B/param + 8 texels of 4 B per coordinate) over the measured step time, and the
     # DRAM traffic the ncu capture saw per step against that
@@ -425,9 +433,9 @@ def run_ours(args):
              "note": "whole fit step: Adam 28 B/param + zeroing 4 B/param + texels 32 B/coordinate over the "
                      "production step time; the L2-bound encode/scatter and the tensor-core MLP add time but "
                      "no algorithmic HBM bytes"}
-    fit_k = ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "adam")
+    fit_k = [k for k in ("step_begin", "encode_fwd", "prep_image", "mlp_tc", "encode_bwd", "adam") if k in kern]
     if all(k in ncu for k in fit_k):
-        dram = sum(ncu[k]["dram_bytes"] for k in fit_k)
+        dram = sum(ncu[k]["dram_bytes"] * kern[k][1] / args.steps for k in fit_k)
         whole.update({"dram_bytes_per_step_cold": dram, "dram_over_algorithmic_cold": dram / alg_step,
                       "dram_source_cold": NCU_CAPTURE + " (sum over the step's kernels, each with a cold L2)"})
     try:   # the same with the L2 left warm between kernels (ncu --cache-control none, 6 consecutive steps)

@@ -847,7 +847,15 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   const bool graphs = st != nullptr && !probing;
   const bool whole = graphs && g_prof_on && steps >= 2;
   const bool cached = graphs && !whole;
-  const bool split = tc && graphs && nchunks == 1 && groups[0].nmodels >= 2 && opts->split_step != 0;
+  // The split step pays where a half's Adam and the other half's MLP take comparable times
+  // (measured: Adam ~6 GB/ms, the MLP ~55 ns per 128-sample tile at one CTA per SM); when
+  // either dominates, the halves' extra kernel tails cost more than the overlap saves and
+  // the one-pipeline step is faster (cfg5's T = 2^22: 45.2 vs 41.8 ms per step; cfg2 at
+  // T = 2^15: 0.80 vs 0.70 ms).
+  const double split_adam_ms = 28.0 * (double)m0->net.nparams * (nmodels / 2) / 6.0e9;
+  const double split_mlp_ms = 55e-6 * ((batch + opts->boundary_batch + 127) / 128) * (nmodels / 2);
+  const bool split = tc && graphs && nchunks == 1 && nmodels >= 2 && opts->split_step != 0 &&
+                     split_adam_ms <= 4.0 * split_mlp_ms && split_mlp_ms <= 4.0 * split_adam_ms;
   const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
   const int per = std::min(nmodels, kMaxGroup);
   const size_t ws_bytes = tc ? lm_workspace_bytes(m0->net, per, Bs) : 0;

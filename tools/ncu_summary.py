@@ -37,10 +37,11 @@ def launches(path, out, cmd):
         a[0] += 1
         a[1] += v
     # (names may carry the inr:: namespace or not, depending on the ncu name base)
-    ours = {k.replace('inr::', ''): v for k, v in agg.items() if k.startswith('inr::') or '_kernel' in k}
+    ours = {k.replace('inr::', ''): v for k, v in agg.items()
+            if k.startswith('inr::') or ('_kernel' in k and 'at::' not in k and 'elementwise' not in k)}
     # one launch of each per fp16 fit step; prep_image also serves the decodes, so the
     # share uses per-launch averages: avg(kernel) / sum of the step kernels' averages
-    stepk = ('step_begin', 'sample_kernel', 'encode_fwd', 'prep_image', 'mlp_fit', 'encode_bwd', 'adam')
+    stepk = ('step_begin', 'sample_kernel', 'encode_fwd', 'prep_image', 'mlp_fit', 'encode_bwd', 'adam')   # (adam_tma too)
     step = sum(v[1] / v[0] for k, v in ours.items() if any(s in k for s in stepk))
     with open(out, 'w') as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised per launch)\n")
