@@ -621,7 +621,7 @@ void launch_adam(const GroupArgs& g, int nmodels, const AdamScalars& as, cudaStr
   if (ctas > 0) {
     // beside the MLP (split fit step): the MLP's shared-memory carveout, so that an SM
     // running the MLP CTA also takes these (a carveout change waits for the SM to drain)
-    const int bx = std::max(1, (ctas + nmodels - 1) / nmodels);
+    const int bx = std::max(1, ctas / nmodels);   // at most ctas in all: one per SM beside the MLP
     if (!as.sparse && !g.md[0].grads_fx) {
       constexpr int kT = 512, kC = 2048, kS = 3;   // 96 KB of operands in flight per CTA
       cudaFuncSetAttribute(adam_tma_kernel<kT, kC, kS>, cudaFuncAttributeMaxDynamicSharedMemorySize,

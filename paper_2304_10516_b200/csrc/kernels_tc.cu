@@ -566,8 +566,9 @@ void launch_mlp_tc(const GroupArgs& g, int nmodels, const FitScalars& fs, const 
   // CTAs per model: fill the machine; in the deterministic mode a fixed count, so
   // that the tiles each CTA accumulates in fp32 TMEM (and hence the exact result)
   // do not depend on how many models share the launch
+  // (ctas > 0: at most ctas in all, so that every CTA has its SM slot beside the side Adam)
   int per_model = fs.det ? std::min(ntiles, kDetCtasPerModel)
-                         : std::max(1, std::min(ntiles, (slots + nmodels - 1) / nmodels));
+                         : std::max(1, std::min(ntiles, ctas > 0 ? slots / nmodels : (slots + nmodels - 1) / nmodels));
   dim3 grid(per_model, nmodels);
   float ls = loss_scale_for(fs.B_u);
   switch (g.net.F * 10 + g.net.D) {
