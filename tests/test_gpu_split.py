@@ -25,15 +25,23 @@ pytestmark = pytest.mark.gpu
 CFG1 = dict(levels=8, features=2, log2_table_size=14, mlp_hidden_layers=2)
 
 
-def _setup(n_models, reduction, seed0=11):
-    vol = synth.g1_analytic(32).numpy()
+def _setup(n_models, reduction, seed0=11, vector=False, sparse=0):
+    if vector:   # D = 3: the Taylor-Green velocity field, per-channel ranges (R28)
+        vol = synth.taylor_green_volume(32, 0.0, amp=2.0).numpy()
+    else:
+        vol = synth.g1_analytic(32).numpy()
     blocks = sampler.decompose((32, 32, 32), (16, 16, 16))[:n_models]
-    lo, hi = sampler.value_range([vol])
     vt = gpu_volume(vol)
-    models = [make_gpu_model(b, seed0 + i, reduction=reduction, precision=inr.INR_PREC_FP16_MLP, **CFG1)
+    kw = dict(CFG1, out_dim=3) if vector else CFG1
+    models = [make_gpu_model(b, seed0 + i, reduction=reduction, precision=inr.INR_PREC_FP16_MLP, **kw)
               for i, b in enumerate(blocks)]
     go = inr.inr_fit_opts_default()
-    go.vmin, go.vmax, go.boundary_batch, go.lr_step = lo, hi, 256, 3
+    if vector:
+        for c in range(3):
+            go.vmin_c[c], go.vmax_c[c] = float(vol[..., c].min()), float(vol[..., c].max())
+    else:
+        go.vmin, go.vmax = sampler.value_range([vol])
+    go.boundary_batch, go.lr_step, go.sparse_adam = 256, 3, sparse
     return vt, models, go
 
 
@@ -43,13 +51,15 @@ def _state(m):
     return p, mm, vv
 
 
-@pytest.mark.parametrize("n_models", [2, 5])
-def test_split_step_bitwise_equals_unsplit_deterministic(n_models):
+@pytest.mark.parametrize("n_models,vector,sparse", [(2, False, 0), (5, False, 0), (4, True, 0), (4, False, 1)],
+                         ids=["2", "5", "4-vector", "4-sparse-adam"])
+def test_split_step_bitwise_equals_unsplit_deterministic(n_models, vector, sparse):
     """5 models: halves of 2 and 3.  Two calls (7 + 4 steps: the first-step and
-    steady-step graphs, the final flush of half B's Adam, LR decays at s = 3, 6, 9)."""
+    steady-step graphs, the final flush of half B's Adam, LR decays at s = 3, 6, 9);
+    also D = 3 vector-field models (R28) and the R37 touched-only Adam beside the MLP."""
     out = []
     for split in (1, 0):
-        vt, models, go = _setup(n_models, reduction=1)
+        vt, models, go = _setup(n_models, reduction=1, vector=vector, sparse=sparse)
         go.split_step = split
         views = [whole_view(vt)] * n_models
         for steps in (7, 4):
