@@ -428,12 +428,22 @@ __global__ void __launch_bounds__(kFitThreads, 2) mlp_fit_kernel(GroupArgs g, Fi
         tmem_wait_ld();
         if (lane < 16) {
           const int n = (warp & 3) * 16 + lane;
+          if (!det && c + 16 <= in) {
+            // 16 weights of row n: four 16-B vector reductions (in and the tensor offset are
+            // multiples of 4 floats)
+            float4* dst = reinterpret_cast<float4*>(G + net.w_off[k] + (size_t)n * in + c);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            int col = c + j;
-            float gval = v[j] * inv_scale;
-            if (col < in) grad_add(G, GX, net.w_off[k] + (size_t)n * in + col, gval);
-            else if (col == in && ones) grad_add(G, GX, net.b_off[k] + n, gval);
+            for (int j = 0; j < 16; j += 4)
+              atomicAdd(dst + j / 4, make_float4(v[j] * inv_scale, v[j + 1] * inv_scale, v[j + 2] * inv_scale,
+                                                 v[j + 3] * inv_scale));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              int col = c + j;
+              float gval = v[j] * inv_scale;
+              if (col < in) grad_add(G, GX, net.w_off[k] + (size_t)n * in + col, gval);
+              else if (col == in && ones) grad_add(G, GX, net.b_off[k] + n, gval);
+            }
           }
         }
       }
