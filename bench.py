@@ -405,6 +405,10 @@ def run_ours(args):
         kernels["mlp_tc"].update({"bound": "tensor", "achieved_tflops": tf,
                                   "peak_tflops": pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
                                   "frac": tf / pk.get("bf16_tflops_sustained", pk["bf16_tflops"])})
+        if mpl.get("mlp_tc", nb) < nb:
+            kernels["mlp_tc"]["note"] = ("split fit step: one CTA per SM beside the other half's Adam, whose longer "
+                                         "HBM-bound launch bounds the phase; the MLP's time is hidden under it "
+                                         "(alone: profiles/r2_ncu_full.txt)")
     try:   # gather / red kernels: L2 sectors per launch (ncu capture) / avg launch vs the measured peaks
         with open(os.path.join(ROOT, "profiles", "r1_l2_peaks.json")) as f:
             lp = {(r["op"], r["buffer_MB"]): r["per_s"] for r in json.load(f)["results"]}
