@@ -170,10 +170,11 @@ INR_API inr_status inr_steps(const inr_model* m, int64_t* steps);
  *   group of 8 table floats (one 32-B sector) received a non-zero gradient this
  *   step; untouched groups keep p, m and v.  MLP parameters stay dense.
  *   split_step != 0 (default 1): a call that fits one launch group of >= 2 fp16
- *   models on a stream without PSNR-target stopping, whose Adam does not
- *   dominate its MLP (not for cfg5's T = 2^22 tables), runs each step as two
- *   halves of the group, and each half's Adam runs beside the other half's
- *   tensor-core MLP ("split fit step").  Every model takes the same
+ *   models whose Adam does not dominate its MLP (not for cfg5's T = 2^22
+ *   tables) runs each step as two halves of the group, and each half's Adam
+ *   runs beside the other half's tensor-core MLP ("split fit
+ *   step"); with PSNR-target stopping the deferred Adam is completed before
+ *   every probe.  Every model takes the same
  *   operations in the same order as with split_step = 0, so the deterministic
  *   reduction mode gives bitwise the same parameters either way. */
 typedef struct {

@@ -852,10 +852,16 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   // either dominates, the halves' extra kernel tails cost more than the overlap saves and
   // the one-pipeline step is faster (cfg5's T = 2^22: 45.2 vs 41.8 ms per step; cfg2 at
   // T = 2^15: 0.80 vs 0.70 ms).
-  const double split_adam_ms = 28.0 * (double)m0->net.nparams * (nmodels / 2) / 6.0e9;
-  const double split_mlp_ms = 55e-6 * ((batch + opts->boundary_batch + 127) / 128) * (nmodels / 2);
-  const bool split = tc && graphs && nchunks == 1 && nmodels >= 2 && opts->split_step != 0 &&
-                     split_adam_ms <= 4.0 * split_mlp_ms && split_mlp_ms <= 4.0 * split_adam_ms;
+  auto split_ok = [&](int nm) {
+    const double adam_ms = 28.0 * (double)m0->net.nparams * (nm / 2) / 6.0e9;
+    const double mlp_ms = 55e-6 * ((batch + opts->boundary_batch + 127) / 128) * (nm / 2);
+    return tc && nchunks == 1 && nm >= 2 && opts->split_step != 0 && adam_ms <= 4.0 * mlp_ms &&
+           mlp_ms <= 4.0 * adam_ms;
+  };
+  const bool split = graphs && split_ok(nmodels);
+  // without graphs (PSNR-target stopping, the legacy stream) the same split step is enqueued
+  // live; half B's deferred Adam is flushed before every probe (which reads the parameters)
+  bool live = !graphs && split_ok(nmodels);
   const int Bs = (batch + opts->boundary_batch + 127) / 128 * 128;
   const int per = std::min(nmodels, kMaxGroup);
   const size_t ws_bytes = tc ? lm_workspace_bytes(m0->net, per, Bs) : 0;
@@ -897,13 +903,16 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   if (tc) ws = lm_workspace(ws_base, m0->net, per, Bs);
   GroupArgs gh[2];
   LmWorkspace wh[2];
-  if (split) {
+  auto set_halves = [&]() {
     const int h = groups[0].nmodels / 2;
     gh[0] = sub_group(groups[0], 0, h);
     gh[1] = sub_group(groups[0], h, groups[0].nmodels - h);
     wh[0] = sub_workspace(ws, m0->net, 0);
     wh[1] = sub_workspace(ws, m0->net, h);
-  }
+  };
+  if (split || live) set_halves();
+  std::unique_ptr<SideStream> live_side(live ? new SideStream() : nullptr);
+  bool live_first = true;   // no deferred Adam pending
   // beside each other: one MLP CTA (256 threads, half the registers) and one TMA-fed Adam
   // CTA (512 threads, 96 KB of operands in flight) per SM
   constexpr int kSplitMlpCtas = 148, kSplitAdamCtas = 148;
@@ -1038,12 +1047,20 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       }
       // (split: 10 launches per step, 9 in a call's first, + the final Adam flush)
       count_launch(split ? (whole ? 10ll * steps : (s == 0 ? 9 : 10)) : (long long)launches_per_step * (whole ? steps : 1));
+    } else if (live) {
+      enqueue_split(st, *live_side, live_first);
+      live_first = false;
+      CK_LAUNCH("fit step");
     } else {
       enqueue_step(st, nullptr);
       CK_LAUNCH("fit step");
     }
     taken = s + 1;
     if (probing && taken % opts->check_interval == 0) {
+      if (live && !live_first) {
+        flush_split(st);
+        live_first = true;
+      }
       for (int c = 0; c < nchunks; ++c)
         for (int j = 0; j < groups[c].nmodels; ++j)
           CK(cudaMemsetAsync(groups[c].md[j].acc + 2, 0, sizeof(double), st));
@@ -1064,10 +1081,13 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       if (still.size() != active.size()) {   // the converged models leave the group
         active.swap(still);
         build_groups();
+        live = live && split_ok((int)active.size());
+        if (live) set_halves();
       }
     }
   }
   if (split && !whole) flush_split(st);   // (counts its own launch)
+  if (live && !live_first) flush_split(st);
   if (exec && !cached) cudaGraphExecDestroy(exec);
   if (exec_first && !cached) cudaGraphExecDestroy(exec_first);
   for (int i = 0; i < nmodels; ++i) {

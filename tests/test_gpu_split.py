@@ -125,3 +125,26 @@ def test_split_step_multistep_matches_unsplit_statistically():
     for x, y in zip(la, lb):
         assert abs(x - y) <= 0.05 * max(x, y), (la, lb)
     assert all(np.isfinite(x).all() for x in pa)
+
+
+def test_live_split_with_psnr_target_stopping_bitwise():
+    """Without CUDA graphs (PSNR-target stopping probes the models every
+    check_interval steps) the split step is enqueued live and half B's deferred
+    Adam is flushed before each probe; models leave the group as they converge
+    (the halves are re-formed).  Deterministic mode: every model's parameters and
+    step count equal the unsplit fit's bitwise."""
+    out = []
+    for split in (1, 0):
+        vt, models, go = _setup(6, reduction=1, seed0=21)
+        go.split_step = split
+        go.target_psnr, go.check_interval = 38.0, 20
+        reps = inr.inr_fit_group(models, [whole_view(vt)] * 6, 200, 1024, go, stream())
+        out.append(([(r.steps_taken, r.reached_target) for r in reps], [_state(m) for m in models]))
+        for m in models:
+            inr.inr_destroy(m)
+    (ra, sa), (rb, sb) = out
+    print("live split, steps / reached:", ra)
+    assert ra == rb and len({s for s, _ in ra}) > 1   # models stop at different checks
+    for x, y in zip(sa, sb):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
