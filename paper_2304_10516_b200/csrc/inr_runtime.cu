@@ -677,7 +677,7 @@ constexpr size_t kGraphCache = 4;
 // A and B run the pipeline in turn, and each half's Adam (HBM-bound) runs on a second
 // stream beside the other half's tensor-core MLP (latency-bound), on the SMs' spare
 // registers and warps:
-//   fwd_A prep_A {mlp_A | adam_B(s-1)} bwd_A fwd_B prep_B {mlp_B | adam_A(s)} bwd_B
+//   fwd_A {mlp_A bwd_A | adam_B(s-1)} fwd_B {mlp_B bwd_B | adam_A(s)}   (prep_X beside fwd_X)
 // Half B's Adam of the last step is flushed at the end of the call.  Per model the
 // order of operations is the unsplit step's (blocks are independent).
 static GroupArgs sub_group(const GroupArgs& g, int j0, int n) {
@@ -941,8 +941,9 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
       { ProfScope p(PK_MLP_TC, s);
         launch_mlp_tc(g, g.nmodels, fs, w.featimg, w.wimg, w.samples, w.targets, w.dfeat, w.Bs, s,
                       side_adam ? kSplitMlpCtas : 0); }
-      if (side_adam) fork(side.s, s, side.ev[4 * hf + 3]);
       { ProfScope p(PK_ENCODE_BWD, s); launch_encode_bwd(g, g.nmodels, fs, w, s); }
+      // (joined after the scatter: the Adam's tail may also run beside this half's scatter)
+      if (side_adam) fork(side.s, s, side.ev[4 * hf + 3]);
     }
   };
   auto flush_split = [&](cudaStream_t s) {   // half B's Adam of the last step
