@@ -673,10 +673,10 @@ static std::list<FitGraph> g_graphs;
 static unsigned long long g_graph_clock = 0;
 constexpr size_t kGraphCache = 4;
 
-// ---- split fit step (one group of >= 2 models, CUDA graphs): the group's two halves
-// A and B run the pipeline in turn, and each half's Adam (HBM-bound) runs on a second
-// stream beside the other half's tensor-core MLP (latency-bound), on the SMs' spare
-// registers and warps:
+// ---- split fit step (one launch group of >= 2 models): the group's two halves A and B
+// run the pipeline in turn, and each half's Adam (HBM-bound) runs on a second stream
+// beside the other half's tensor-core MLP (latency-bound), on the SMs' spare registers
+// and warps, its tail beside the start of that half's scatter:
 //   fwd_A {mlp_A bwd_A | adam_B(s-1)} fwd_B {mlp_B bwd_B | adam_A(s)}   (prep_X beside fwd_X)
 // Half B's Adam of the last step is flushed at the end of the call.  Per model the
 // order of operations is the unsplit step's (blocks are independent).
@@ -699,7 +699,8 @@ static LmWorkspace sub_workspace(const LmWorkspace& w, const NetDesc& net, int j
   return s;
 }
 
-// the side stream and fork / join events of the split step while it is captured
+// the side stream and fork / join events of the split step (for a capture, or for one
+// call's live steps)
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t ev[8] = {};
