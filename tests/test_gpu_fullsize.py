@@ -13,7 +13,7 @@ import pytest
 import torch
 
 import synth
-from oracle import decode as o_decode, fit as o_fit, sampler
+from oracle import adam as o_adam, decode as o_decode, fit as o_fit, sampler
 from oracle.model import InrModel
 from paper_2304_10516_b200 import inr
 
@@ -137,5 +137,16 @@ def test_fullsize_group_step_gradients(g2, prec):
             r /= 2.0 ** -11
             print(f"fp16 full-size group block {bi} componentwise err / (u g_abs)", r)
             assert r <= 2 * (cfg.mlp_hidden_layers + 2)
+        # the step's Adam (t = 1) on the GPU's own gradient, element by element: in the fp16
+        # launch the split step updates block 0 with the TMA-fed Adam beside the other
+        # half's MLP and block 7 with the call's final flush
+        pe = p0.astype(np.float64)
+        o_adam.adam_update(pe, g.astype(np.float64), np.zeros_like(pe), np.zeros_like(pe), 1,
+                           o_adam.lr_at(0, 1e-2, 0.8, 500))
+        pg = get_params(ms[bi]).astype(np.float64)
+        tol = 1e-6 * 1e-2 + 2.0 ** -21 * np.abs(pe)
+        ratio = float(np.max(np.abs(pg - pe) / tol))
+        print(f"full-size group block {bi} Adam error / tolerance", ratio)
+        assert ratio <= 1
     for m in ms:
         inr.inr_destroy(m)
