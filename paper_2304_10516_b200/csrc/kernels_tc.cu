@@ -720,13 +720,17 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
   // (MODE 3: tiles grouped by block, so one or two blocks' weights at a time); a
   // CTA reloads the weight image only when its next tile belongs to another block
   long long t0 = blockIdx.x, t1;
+  // MODE 1: tile = 8 super-brick + sub-brick; a CTA takes the 8 bricks of one 2 x 2 x 2
+  // super-brick in a row (their coarse levels staged once), then jumps gridDim.x on
+  const int nbx = (a.cnt[0] + kBrickX - 1) / kBrickX, nby = (a.cnt[1] + kBrickY - 1) / kBrickY,
+            nbz = (a.cnt[2] + kBrickZ - 1) / kBrickZ;
+  const int nsx = (nbx + kSupX - 1) / kSupX, nsy = (nby + kSupY - 1) / kSupY, nsz = (nbz + kSupZ - 1) / kSupZ;
   if constexpr (MODE == 0) t1 = (a.q + kTileM - 1) / kTileM;
-  else if constexpr (MODE == 1)
-    t1 = (long long)((a.cnt[0] + kBrickX - 1) / kBrickX) * ((a.cnt[1] + kBrickY - 1) / kBrickY) *
-         ((a.cnt[2] + kBrickZ - 1) / kBrickZ);
+  else if constexpr (MODE == 1) { t0 *= kSubs; t1 = (long long)kSubs * nsx * nsy * nsz; }
   else { t0 += a.tile0; t1 = min(a.tile1, (long long)*a.ntiles_dev); }
   const long long tstep = gridDim.x;
-  for (long long tile = t0; tile < t1; tile += tstep) {
+  for (long long tile = t0; tile < t1;
+       tile = MODE == 1 ? (tile % kSubs == kSubs - 1 ? tile + kSubs * (tstep - 1) + 1 : tile + 1) : tile + tstep) {
     const int slot = MODE == 3 ? a.tile_slot[tile] : 0;
     if (slot != cur) {   // one TMA bulk copy of this block's prepared weight image
       __syncthreads();
@@ -748,12 +752,14 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
       valid = j < a.q;
       if (valid) { x[0] = __ldg(a.x01 + 3 * j); x[1] = __ldg(a.x01 + 3 * j + 1); x[2] = __ldg(a.x01 + 3 * j + 2); }
     } else if constexpr (MODE == 1) {
-      // brick (bx, by, bz) of 8 x 4 x 4 lattice points; points past cnt are computed
-      // at the clamped (last) lattice point and not stored
-      // (32-bit: a grid whose output fits in device memory has < 2^31 bricks)
-      const unsigned nbx = (a.cnt[0] + kBrickX - 1) / kBrickX, nby = (a.cnt[1] + kBrickY - 1) / kBrickY;
-      const unsigned tu = (unsigned)tile, rr = tu / nbx;
-      const int bx = (int)(tu - rr * nbx), by = (int)(rr % nby), bz = (int)(rr / nby);
+      // brick (bx, by, bz) of 8 x 4 x 4 lattice points, sub-brick (tile & 7) of super-brick
+      // tile >> 3; points past cnt are computed at the clamped (last) lattice point and not
+      // stored (32-bit: a grid whose output fits in device memory has < 2^31 bricks)
+      const unsigned su = (unsigned)(tile / kSubs), sr = su / (unsigned)nsx;
+      const int sx = (int)(su - sr * nsx), sy = (int)(sr % (unsigned)nsy), sz = (int)(sr / (unsigned)nsy);
+      const int sub = (int)(tile % kSubs);
+      const int bx = kSupX * sx + sub % kSupX, by = kSupY * sy + (sub / kSupX) % kSupY, bz = kSupZ * sz + sub / (kSupX * kSupY);
+      if (bx >= nbx || by >= nby || bz >= nbz) continue;   // (uniform over the CTA)
       const int jx = bx * kBrickX + (r & 7), jy = by * kBrickY + ((r >> 3) & 3), jz = bz * kBrickZ + (r >> 5);
       valid = jx < a.cnt[0] && jy < a.cnt[1] && jz < a.cnt[2];
       const int jj[3] = {min(jx, a.cnt[0] - 1), min(jy, a.cnt[1] - 1), min(jz, a.cnt[2] - 1)};
@@ -765,14 +771,14 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
         for (int d = 0; d < 3; ++d) x[d] = mesh_x(md, d, md.mesh[d][min(jj[d], md.mesh_n[d] - 1)]);
       }
       dst = jx * a.os[0] + jy * a.os[1] + jz * a.os[2];
-      if (a.nst > 0 && t < 32) {
-        // the brick's vertex box per staged level (lane l: level l): lo / n per axis from
-        // the brick's first and last lattice point, with level_cell's pinned arithmetic
+      if (sub == 0 && a.nst > 0 && t < 32) {
+        // the super-brick's vertex box per staged level (lane l: level l): lo / n per axis from
+        // its first and last lattice point, with level_cell's pinned arithmetic
         int* box = reinterpret_cast<int*>(smem + lay.stbox);
         if (t < a.nst) {
-          const int b0[3] = {bx * kBrickX, by * kBrickY, bz * kBrickZ};
-          const int b1[3] = {min(b0[0] + kBrickX, a.cnt[0]) - 1, min(b0[1] + kBrickY, a.cnt[1]) - 1,
-                             min(b0[2] + kBrickZ, a.cnt[2]) - 1};
+          const int b0[3] = {sx * kSupX * kBrickX, sy * kSupY * kBrickY, sz * kSupZ * kBrickZ};
+          const int b1[3] = {min(b0[0] + kSupX * kBrickX, a.cnt[0]) - 1, min(b0[1] + kSupY * kBrickY, a.cnt[1]) - 1,
+                             min(b0[2] + kSupZ * kBrickZ, a.cnt[2]) - 1};
           const uint32_t res = net.lv[t].res;
           int lo[3], n[3];
 #pragma unroll
@@ -836,7 +842,7 @@ __global__ void __launch_bounds__(kFwdThreads, 4) forward_tc_kernel(GroupArgs g,
             }
         };
         issue(lf0);
-        if (a.nst > 0) {
+        if (a.nst > 0 && (MODE != 1 || tile % kSubs == 0)) {   // (MODE 1: once per super-brick)
           // stage the staged levels' vertex boxes: one entry per thread over the
           // concatenated boxes (every load in flight at once, with the fine gathers above)
           __syncthreads();   // the box table
@@ -1026,7 +1032,7 @@ void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res
   a.sse = sse;
   // staged levels: the coarse levels (N_l < R on every axis) whose worst-case vertex
   // box per brick, (ceil((B_d - 1) N_l / R_d) + 2) per axis, fits the stage area
-  const int B[3] = {kBrickX, kBrickY, kBrickZ};
+  const int B[3] = {kSupX * kBrickX, kSupY * kBrickY, kSupZ * kBrickZ};   // the staged super-brick
   int off = 0;
   a.nst = 0;
   a.st_off[0] = 0;
@@ -1054,9 +1060,10 @@ void launch_decode_grid_tc(const NetDesc& net, const ModelDev& md, const int res
     a.na = l;
   }
   for (int d = 0; d < 3; ++d) a.rinv[d] = (res[d] & (res[d] - 1)) == 0 ? 1.f / (float)res[d] : 0.f;
-  const long long nb = (long long)((cnt[0] + kBrickX - 1) / kBrickX) * ((cnt[1] + kBrickY - 1) / kBrickY) *
-                       ((cnt[2] + kBrickZ - 1) / kBrickZ);
-  launch_forward<1>(*single_group(net, md), a, nb, st);
+  const long long nbx = (cnt[0] + kBrickX - 1) / kBrickX, nby = (cnt[1] + kBrickY - 1) / kBrickY,
+                  nbz = (cnt[2] + kBrickZ - 1) / kBrickZ;
+  const long long nsb = ((nbx + kSupX - 1) / kSupX) * ((nby + kSupY - 1) / kSupY) * ((nbz + kSupZ - 1) / kSupZ);
+  launch_forward<1>(*single_group(net, md), a, nsb, st);
 }
 
 // Queries: per chunk of <= 2^15 bucketed tiles, x per query (query_prep_kernel),

@@ -17,7 +17,10 @@ constexpr int kThreads = 128;
 constexpr int kTileM = 128;
 // grid decode tiles are 8 x 4 x 4 bricks of lattice points (thread t <-> (t & 7, (t >> 3) & 3, t >> 5))
 constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4;
-constexpr int kStageFloats = 640;    // smem floats for the staged coarse-level vertices of one brick
+constexpr int kStageFloats = 1536;   // smem floats for the staged coarse-level vertices of one super-brick
+// grid decode: a CTA stages the coarse levels once per super-brick of kSupX x kSupY x kSupZ bricks
+// (measured: 2 x 2 x 2 beats 1 x 2 x 2, 2 x 2 x 1, 4 x 2 x 2 and 4 x 4 x 2)
+constexpr int kSupX = 2, kSupY = 2, kSupZ = 2, kSubs = kSupX * kSupY * kSupZ;
 constexpr int kFwdThreads = 256;     // forward-only kernel: thread t <-> row t % 128, column / level half t / 128
 
 struct Layout {
