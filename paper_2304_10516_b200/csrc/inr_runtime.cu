@@ -916,7 +916,10 @@ static inr_status fit_impl(inr_model* const* models, const inr_view* views, int3
   bool live_first = true;   // no deferred Adam pending
   // beside each other: one MLP CTA (256 threads, half the registers) and one TMA-fed Adam
   // CTA (512 threads, 96 KB of operands in flight) per SM
-  constexpr int kSplitMlpCtas = 148, kSplitAdamCtas = 148;
+  // (the device's SM count: 148 on B200)
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m0->device);
+  const int kSplitMlpCtas = nsm, kSplitAdamCtas = nsm;
   // fork / join between the launching stream and the side stream (inside a capture)
   auto fork = [](cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
     cudaEventRecord(e, from);
