@@ -85,6 +85,19 @@ def test_fullsize_decode_sampled(g2):
     ref = o_decode.denormalize(y[:, 0], lo, hi)
     got = out.cpu().numpy()[j[:, 2], j[:, 1], j[:, 0]]
     assert normwise(got, ref) <= 2e-3
+    # grid at 2x (res 256: the staged 2 x 2 x 2 super-bricks cover more coarse levels) against
+    # the same points decoded as queries (o + j / 2 in node units: x = j / 256 exactly), bitwise
+    out2 = torch.empty((2 * BLOCK,) * 3, device="cuda")
+    inr.inr_decode_grid(gms[6], (2 * BLOCK,) * 3, out2.data_ptr(), None, None, None, stream())
+    j2 = rng.integers(0, 2 * BLOCK, size=(50000, 3))
+    o6 = np.array(blocks[6].origin, dtype=np.float32)
+    p2 = (o6[None, :] + j2.astype(np.float32) * np.float32(0.5)).astype(np.float32)
+    p2d = torch.from_numpy(p2).cuda()
+    q2 = torch.empty(p2.shape[0], device="cuda")
+    inr.inr_decode_group([gms[6]], p2d.data_ptr(), p2.shape[0], q2.data_ptr(), 0, stream())
+    torch.cuda.synchronize()
+    g2x = out2.cpu().numpy()[j2[:, 2], j2[:, 1], j2[:, 0]]
+    assert np.array_equal(g2x, q2.cpu().numpy())
     # queries: bench's launch (all of the rank's blocks, bucketed, tensor-core MLP)
     pts = synth.random_points(1 << 16, g2.shape[::-1])
     pd = torch.from_numpy(pts).cuda()
